@@ -1,0 +1,1028 @@
+// otdr_dev.cu -- C-ABI (include/otdr_dev.h) over the sm_100a RDROT kernels.
+//
+// Host side of the drop-in boundary: owns device memory, the stream, CUDA
+// graphs and (row-sharded runs) the NCCL communicator. The solve loop of
+// solver.cpp:104-241 runs entirely on device: one CUDA graph whose WHILE
+// conditional node repeats a body of `unroll` DR iterations until the update
+// kernel clears the condition (converged / stalled / max_iter / non-finite).
+// Multi-rank contexts (NCCL inside the body) use host-polled chunk graphs.
+#include "otdr_dev.h"
+#include "otdr_kernels.cuh"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <numeric>
+#include <string>
+#include <tuple>
+#include <vector>
+
+using otdrk::Ctl;
+using otdrk::Params;
+using otdrk::Segment;
+
+namespace {
+
+constexpr int kNumSMs = 148;
+constexpr int kSweepTN = 256;  // plain sweep stripe width (both storages)
+constexpr size_t kStageDoubles = size_t(1) << 25;  // 256 MB fp64 staging
+
+struct Error {
+  otdr_status code;
+  std::string msg;
+};
+
+#define CK(expr)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      throw Error{OTDR_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)};   \
+  } while (0)
+#define NK(expr)                                                                      \
+  do {                                                                                \
+    ncclResult_t r_ = (expr);                                                         \
+    if (r_ != ncclSuccess)                                                            \
+      throw Error{OTDR_E_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)};   \
+  } while (0)
+
+template <typename T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  CK(cudaMalloc(&p, count * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+}  // namespace
+
+struct otdr_dev {
+  otdr_dev_config cfg{};
+  int storage = OTDR_STORE_F32;
+  size_t esz = 4;
+  long long m_glob = 0, n = 0, m_loc = 0, row0 = 0, ld = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  ncclComm_t comm = nullptr;
+  std::string err;
+
+  void* C = nullptr;
+  void* X = nullptr;
+  double *p = nullptr, *q = nullptr, *phi = nullptr, *psi = nullptr, *a = nullptr, *b = nullptr,
+         *r = nullptr, *s = nullptr;
+  double *rowpart = nullptr, *colpart = nullptr, *exch = nullptr, *bpart = nullptr,
+         *cpart = nullptr, *csum = nullptr, *stage = nullptr;
+  long long* d_dev_row = nullptr;
+  Segment *d_seg = nullptr, *d_cert_seg = nullptr;
+  Params* d_prm = nullptr;
+  Ctl* d_ctl = nullptr;
+  Ctl* h_ctl = nullptr;  // pinned
+  otdrk::TraceRow* d_trace = nullptr;
+  long long trace_cap = 0;
+  unsigned long long* d_mx = nullptr;
+
+  // host mirrors
+  Params prm{};
+  std::vector<long long> dev_row;  // host (local) row -> device row
+  std::vector<double> h_p, h_q;
+  std::vector<int32_t> labels;
+  int reg_kind = OTDR_REG_NONE;
+  double reg_param = 0.0;
+  bool has_problem = false, has_state = false;
+
+  // geometry
+  int stripes = 1, rowgroups = 1, rows_per_cta = 1;
+  int gl_stripes = 1, num_segs = 0, cert_stripes = 1, num_cert_segs = 0;
+  int RB = 1, CB = 1;
+  size_t rowpart_cap = 0, colpart_cap = 0, cpart_cap = 0;
+  std::vector<Segment> segs, cert_segs;
+
+  // graphs keyed by (kind, unroll/chunk, track, cert)
+  std::map<std::tuple<int, int, int, int>, cudaGraphExec_t> graphs;
+
+  bool f64() const { return storage == OTDR_STORE_F64; }
+  int tn_seg() const { return f64() ? 64 : 128; }  // GL / certificate stripe width
+
+  // ---------------------------------------------------------------- launches
+  void launch_sweep(bool track, bool sums_only) {
+    if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only) {
+      dim3 grid(gl_stripes, num_segs);
+      if (f64()) {
+        otdrk::GLArgs<double> ga{(double*)X, (const double*)C, phi, psi, rowpart, colpart,
+                                 d_seg, d_prm, d_ctl, m_loc, ld};
+        if (track) otdrk::gl_sweep_kernel<double, true, true, 1><<<grid, otdrk::kThreads, 0, stream>>>(ga);
+        else otdrk::gl_sweep_kernel<double, true, false, 1><<<grid, otdrk::kThreads, 0, stream>>>(ga);
+      } else {
+        otdrk::GLArgs<float> ga{(float*)X, (const float*)C, phi, psi, rowpart, colpart,
+                                d_seg, d_prm, d_ctl, m_loc, ld};
+        if (track) otdrk::gl_sweep_kernel<float, false, true, 1><<<grid, otdrk::kThreads, 0, stream>>>(ga);
+        else otdrk::gl_sweep_kernel<float, false, false, 1><<<grid, otdrk::kThreads, 0, stream>>>(ga);
+      }
+      return;
+    }
+    dim3 grid(stripes, rowgroups);
+    const int so = sums_only ? 1 : 0;
+    if (f64()) {
+      otdrk::SweepArgs<double> sa{(double*)X, (const double*)C, phi, psi, rowpart, colpart,
+                                  d_prm, d_ctl, m_loc, ld, rows_per_cta, so};
+      if (reg_kind == OTDR_REG_QUAD) {
+        if (track) otdrk::sweep_kernel<double, otdrk::REG_QUAD, true, true, 4, 1><<<grid, otdrk::kThreads, 0, stream>>>(sa);
+        else otdrk::sweep_kernel<double, otdrk::REG_QUAD, true, false, 4, 1><<<grid, otdrk::kThreads, 0, stream>>>(sa);
+      } else {
+        if (track) otdrk::sweep_kernel<double, otdrk::REG_NONE, true, true, 4, 1><<<grid, otdrk::kThreads, 0, stream>>>(sa);
+        else otdrk::sweep_kernel<double, otdrk::REG_NONE, true, false, 4, 1><<<grid, otdrk::kThreads, 0, stream>>>(sa);
+      }
+    } else {
+      otdrk::SweepArgs<float> sa{(float*)X, (const float*)C, phi, psi, rowpart, colpart,
+                                 d_prm, d_ctl, m_loc, ld, rows_per_cta, so};
+      if (reg_kind == OTDR_REG_QUAD) {
+        if (track) otdrk::sweep_kernel<float, otdrk::REG_QUAD, false, true, 2, 2><<<grid, otdrk::kThreads, 0, stream>>>(sa);
+        else otdrk::sweep_kernel<float, otdrk::REG_QUAD, false, false, 2, 2><<<grid, otdrk::kThreads, 0, stream>>>(sa);
+      } else {
+        if (track) otdrk::sweep_kernel<float, otdrk::REG_NONE, false, true, 2, 2><<<grid, otdrk::kThreads, 0, stream>>>(sa);
+        else otdrk::sweep_kernel<float, otdrk::REG_NONE, false, false, 2, 2><<<grid, otdrk::kThreads, 0, stream>>>(sa);
+      }
+    }
+  }
+
+  bool gl_active(bool sums_only) const { return reg_kind == OTDR_REG_GROUP_LASSO && !sums_only; }
+
+  void launch_reduce(bool sums_only) {
+    otdrk::ReduceArgs ra{rowpart, colpart, p, r, exch, bpart, d_ctl, m_loc, n, ld,
+                         gl_active(sums_only) ? gl_stripes : stripes,
+                         gl_active(sums_only) ? num_segs : rowgroups, RB};
+    otdrk::reduce_kernel<<<RB + CB, otdrk::kThreads, 0, stream>>>(ra);
+  }
+
+  void launch_exchange(double* buf, size_t count) {
+    if (comm) NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, comm, stream));
+  }
+
+  void launch_update(cudaGraphConditionalHandle cond, int use_cond, int cert_follows) {
+    otdrk::UpdateArgs ua{exch, q, r, s, phi, psi, a, b, bpart, d_prm, d_ctl, d_trace,
+                         m_loc, m_glob, n, RB, CB, cond, use_cond, cert_follows};
+    otdrk::update_kernel<<<RB + CB, otdrk::kThreads, 0, stream>>>(ua);
+  }
+
+  void launch_cert(int objective_only, cudaGraphConditionalHandle cond, int use_cond) {
+    const int regk = reg_kind == OTDR_REG_GROUP_LASSO ? otdrk::REG_GL
+                     : reg_kind == OTDR_REG_QUAD      ? otdrk::REG_QUAD
+                                                      : otdrk::REG_NONE;
+    dim3 grid(cert_stripes, num_cert_segs);
+    if (f64()) {
+      otdrk::CertArgs<double> ca{(const double*)X, (const double*)C, phi, psi, p, d_cert_seg,
+                                 cpart, csum, d_prm, d_ctl, m_loc, ld, regk, objective_only};
+      otdrk::cert_partial_kernel<double, 1><<<grid, otdrk::kThreads, 0, stream>>>(ca);
+    } else {
+      otdrk::CertArgs<float> ca{(const float*)X, (const float*)C, phi, psi, p, d_cert_seg,
+                                cpart, csum, d_prm, d_ctl, m_loc, ld, regk, objective_only};
+      otdrk::cert_partial_kernel<float, 1><<<grid, otdrk::kThreads, 0, stream>>>(ca);
+    }
+    launch_exchange(csum, otdrk::kCertVals);
+    otdrk::CertFinalArgs fa{csum, q, psi, d_prm, d_ctl, d_trace, n, regk, objective_only,
+                            cond, use_cond};
+    otdrk::cert_final_kernel<<<1, otdrk::kThreads, 0, stream>>>(fa);
+  }
+
+  // One DR iteration: sweep, reduce, [all-reduce], update, [certificate].
+  void launch_iteration(bool track, bool cert, cudaGraphConditionalHandle cond, int use_cond) {
+    launch_sweep(track, false);
+    launch_reduce(false);
+    launch_exchange(exch, size_t(n) + 3);
+    launch_update(cond, use_cond, cert ? 1 : 0);
+    if (cert) launch_cert(0, cond, use_cond);
+  }
+
+  void check_launch() { CK(cudaGetLastError()); }
+
+  // ---------------------------------------------------------------- geometry
+  void plan_geometry() {
+    stripes = int((ld + kSweepTN - 1) / kSweepTN);
+    const long long target = 8LL * 2 * kNumSMs;  // ~8 waves at 2 CTAs/SM
+    long long rg = std::max<long long>(1, target / stripes);
+    rg = std::min<long long>(rg, std::max<long long>(1, (m_loc + 15) / 16));
+    rows_per_cta = int((m_loc + rg - 1) / rg);
+    rowgroups = int((m_loc + rows_per_cta - 1) / rows_per_cta);
+    gl_stripes = int((ld + tn_seg() - 1) / tn_seg());
+    cert_stripes = gl_stripes;
+    RB = int((m_loc + otdrk::kThreads - 1) / otdrk::kThreads);
+    CB = int((n + otdrk::kThreads - 1) / otdrk::kThreads);
+  }
+
+  // Segments for the group-lasso sweep (class runs in device order) and the
+  // certificate (class runs for GL; uniform row chunks otherwise).
+  void build_segments() {
+    segs.clear();
+    cert_segs.clear();
+    if (reg_kind == OTDR_REG_GROUP_LASSO) {
+      std::vector<int32_t> dev_lab(static_cast<size_t>(m_loc));
+      for (long long h = 0; h < m_loc; ++h) dev_lab[size_t(dev_row[h])] = labels[size_t(h)];
+      long long i = 0;
+      while (i < m_loc) {
+        long long j = i;
+        while (j < m_loc && dev_lab[size_t(j)] == dev_lab[size_t(i)]) ++j;
+        const int grouped = dev_lab[size_t(i)] >= 0 ? 1 : 0;
+        if (grouped) {
+          segs.push_back(Segment{i, j, 1, 0});
+          cert_segs.push_back(Segment{i, j, 1, 0});
+        } else {
+          for (long long t = i; t < j; t += 256) {
+            segs.push_back(Segment{t, std::min(j, t + 256), 0, 0});
+            cert_segs.push_back(Segment{t, std::min(j, t + 256), 0, 0});
+          }
+        }
+        i = j;
+      }
+    } else {
+      const long long chunk = std::max<long long>(64, (m_loc + 63) / 64);
+      for (long long t = 0; t < m_loc; t += chunk)
+        cert_segs.push_back(Segment{t, std::min(m_loc, t + chunk), 0, 0});
+    }
+    if (segs.empty()) segs.push_back(Segment{0, 0, 0, 0});
+    if (cert_segs.empty()) cert_segs.push_back(Segment{0, 0, 0, 0});
+    num_segs = int(segs.size());
+    num_cert_segs = int(cert_segs.size());
+    if (d_seg) cudaFree(d_seg);
+    if (d_cert_seg) cudaFree(d_cert_seg);
+    d_seg = dalloc<Segment>(segs.size());
+    d_cert_seg = dalloc<Segment>(cert_segs.size());
+    CK(cudaMemcpy(d_seg, segs.data(), segs.size() * sizeof(Segment), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_cert_seg, cert_segs.data(), cert_segs.size() * sizeof(Segment),
+                  cudaMemcpyHostToDevice));
+    ensure_partials();
+  }
+
+  void ensure_partials() {
+    const size_t need_row = size_t(std::max(stripes, gl_stripes)) * size_t(std::max<long long>(m_loc, 1));
+    const size_t need_col = size_t(std::max(rowgroups, num_segs)) * size_t(ld);
+    const size_t need_c = size_t(cert_stripes) * size_t(num_cert_segs) * otdrk::kCertVals;
+    if (need_row > rowpart_cap) {
+      if (rowpart) cudaFree(rowpart);
+      rowpart = dalloc<double>(need_row);
+      rowpart_cap = need_row;
+    }
+    if (need_col > colpart_cap) {
+      if (colpart) cudaFree(colpart);
+      colpart = dalloc<double>(need_col);
+      colpart_cap = need_col;
+    }
+    if (need_c > cpart_cap) {
+      if (cpart) cudaFree(cpart);
+      cpart = dalloc<double>(need_c);
+      cpart_cap = need_c;
+    }
+  }
+
+  void invalidate_graphs() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    graphs.clear();
+  }
+
+  // ---------------------------------------------------------------- ctl I/O
+  void pull_ctl() {
+    CK(cudaMemcpyAsync(h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+  }
+  void push_ctl() {
+    CK(cudaMemcpyAsync(d_ctl, h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, stream));
+  }
+  void push_prm() {
+    CK(cudaMemcpyAsync(d_prm, &prm, sizeof(Params), cudaMemcpyHostToDevice, stream));
+    CK(cudaStreamSynchronize(stream));  // prm is a host member reused by later calls
+  }
+
+  void set_rho_params(double rho) {
+    prm.rho = rho;
+    prm.alpha = reg_kind == OTDR_REG_QUAD ? reg_param : 0.0;
+    prm.lambda = reg_kind == OTDR_REG_GROUP_LASSO ? reg_param : 0.0;
+    prm.quad_d = 1.0 + rho * prm.alpha;
+    prm.quad_inv = 1.0 / prm.quad_d;
+    prm.gl_thr = rho * prm.lambda;
+  }
+
+  // ---------------------------------------------------------------- graphs
+  // kind 0: plain chunk of `count` iterations; kind 1: WHILE loop whose body
+  // is `count` iterations.
+  cudaGraphExec_t get_graph(int kind, int count, bool track, bool cert) {
+    auto key = std::make_tuple(kind, count, track ? 1 : 0, cert ? 1 : 0);
+    auto it = graphs.find(key);
+    if (it != graphs.end()) return it->second;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ex = nullptr;
+    if (kind == 0) {
+      CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      for (int t = 0; t < count; ++t) launch_iteration(track, cert, 0, 0);
+      CK(cudaStreamEndCapture(stream, &g));
+    } else {
+      CK(cudaGraphCreate(&g, 0));
+      cudaGraphConditionalHandle h;
+      CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams np{};
+      np.type = cudaGraphNodeTypeConditional;
+      np.conditional.handle = h;
+      np.conditional.type = cudaGraphCondTypeWhile;
+      np.conditional.size = 1;
+      cudaGraphNode_t node;
+      CK(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+      cudaGraph_t body = np.conditional.phGraph_out[0];
+      CK(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0,
+                                       cudaStreamCaptureModeThreadLocal));
+      for (int t = 0; t < count; ++t) launch_iteration(track, cert, h, 1);
+      CK(cudaStreamEndCapture(stream, &body));
+    }
+    CK(cudaGraphInstantiate(&ex, g, 0));
+    CK(cudaGraphDestroy(g));
+    graphs[key] = ex;
+    return ex;
+  }
+
+  // Raw iterations (step): graph chunks plus a directly launched remainder.
+  void run_raw(long long iters) {
+    const int chunk = 16;
+    if (iters >= chunk) {
+      cudaGraphExec_t ex = get_graph(0, chunk, false, false);
+      for (long long t = 0; t + chunk <= iters; t += chunk) CK(cudaGraphLaunch(ex, stream));
+    }
+    for (long long t = 0; t < iters % chunk; ++t) launch_iteration(false, false, 0, 0);
+    check_launch();
+  }
+
+  // ---------------------------------------------------------------- upload
+  template <typename T>
+  void upload_rows(T* dst, const double* src_rows) {
+    if (m_loc == 0) return;
+    const long long rows_per = std::max<long long>(1, (long long)(kStageDoubles / size_t(n)));
+    for (long long r0 = 0; r0 < m_loc; r0 += rows_per) {
+      const long long rows = std::min(rows_per, m_loc - r0);
+      CK(cudaMemcpyAsync(stage, src_rows + r0 * n, size_t(rows * n) * sizeof(double),
+                         cudaMemcpyHostToDevice, stream));
+      otdrk::scatter_rows_kernel<T><<<4 * kNumSMs, 256, 0, stream>>>(dst, stage, d_dev_row + r0,
+                                                                      rows, n, ld);
+      check_launch();
+    }
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  template <typename T>
+  void download_rows(double* dst_rows, const T* src) {
+    if (m_loc == 0) return;
+    const long long rows_per = std::max<long long>(1, (long long)(kStageDoubles / size_t(n)));
+    for (long long r0 = 0; r0 < m_loc; r0 += rows_per) {
+      const long long rows = std::min(rows_per, m_loc - r0);
+      otdrk::gather_rows_kernel<T><<<4 * kNumSMs, 256, 0, stream>>>(stage, src, d_dev_row + r0,
+                                                                     rows, n, ld);
+      check_launch();
+      CK(cudaMemcpyAsync(dst_rows + r0 * n, stage, size_t(rows * n) * sizeof(double),
+                         cudaMemcpyDeviceToHost, stream));
+    }
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  void upload_vec_rows(double* dst, const double* host_order) {
+    std::vector<double> tmp(size_t(std::max<long long>(m_loc, 1)));
+    for (long long h = 0; h < m_loc; ++h) tmp[size_t(dev_row[h])] = host_order[h];
+    CK(cudaMemcpy(dst, tmp.data(), size_t(m_loc) * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  void download_vec_rows(double* host_order, const double* src) {
+    std::vector<double> tmp(size_t(std::max<long long>(m_loc, 1)));
+    CK(cudaMemcpy(tmp.data(), src, size_t(m_loc) * sizeof(double), cudaMemcpyDeviceToHost));
+    for (long long h = 0; h < m_loc; ++h) host_order[h] = tmp[size_t(dev_row[h])];
+  }
+
+  // Re-order device rows of C (and p) when the GL class permutation changes.
+  void permute_rows(const std::vector<long long>& new_row) {
+    if (new_row == dev_row) return;
+    if (has_problem) {
+      void* tmp = nullptr;
+      const size_t bytes = size_t(m_loc) * size_t(ld) * esz;
+      CK(cudaMalloc(&tmp, bytes));
+      long long* d_new = dalloc<long long>(size_t(m_loc));
+      CK(cudaMemcpy(d_new, new_row.data(), size_t(m_loc) * 8, cudaMemcpyHostToDevice));
+      const long long units = ld * (long long)esz / 16;
+      otdrk::move_rows_kernel<<<4 * kNumSMs, 256, 0, stream>>>(
+          static_cast<uint4*>(tmp), static_cast<const uint4*>(C), d_new, d_dev_row, m_loc, units);
+      check_launch();
+      CK(cudaStreamSynchronize(stream));
+      cudaFree(d_new);
+      CK(cudaFree(C));
+      C = tmp;
+      invalidate_graphs();
+    }
+    dev_row = new_row;
+    CK(cudaMemcpy(d_dev_row, dev_row.data(), size_t(m_loc) * sizeof(long long),
+                  cudaMemcpyHostToDevice));
+    if (has_problem) upload_vec_rows(p, h_p.data());
+    has_state = false;
+  }
+
+  // make_state from the X currently in the X buffer and phi/psi buffers.
+  void seed_state() {
+    CK(cudaMemsetAsync(d_ctl, 0, sizeof(Ctl), stream));
+    prm.solving = 0;
+    prm.fused = 0;
+    push_prm();
+    launch_sweep(false, true);
+    launch_reduce(true);
+    launch_exchange(exch, size_t(n) + 3);
+    otdrk::SeedArgs sa{exch, q, r, phi, psi, s, a, b, d_ctl, m_loc, m_glob, n};
+    const long long cnt = std::max(m_loc, n);
+    otdrk::seed_state_kernel<<<int((cnt + 255) / 256), 256, 0, stream>>>(sa);
+    check_launch();
+    CK(cudaStreamSynchronize(stream));
+    has_state = true;
+  }
+
+  void release() {
+    invalidate_graphs();
+    void* ptrs[] = {C, X, p, q, phi, psi, a, b, r, s, rowpart, colpart, exch, bpart, cpart,
+                    csum, stage, d_dev_row, d_seg, d_cert_seg, d_prm, d_ctl, d_trace, d_mx};
+    for (void* ptr : ptrs)
+      if (ptr) cudaFree(ptr);
+    if (h_ctl) cudaFreeHost(h_ctl);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+    if (comm) ncclCommDestroy(comm);
+  }
+};
+
+namespace {
+
+otdr_status fail(otdr_dev* ctx, otdr_status code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+template <typename F>
+otdr_status guarded(otdr_dev* ctx, F&& f) {
+  try {
+    if (ctx) CK(cudaSetDevice(ctx->cfg.device));
+    return f();
+  } catch (const Error& e) {
+    return fail(ctx, e.code, e.msg);
+  } catch (const std::exception& e) {
+    return fail(ctx, OTDR_E_CUDA, e.what());
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int otdr_dev_abi_version(void) { return OTDR_DEV_ABI_VERSION; }
+
+int otdr_dev_cuda_available(void) {
+  int count = 0;
+  return cudaGetDeviceCount(&count) == cudaSuccess && count > 0 ? 1 : 0;
+}
+
+const char* otdr_dev_last_error(const otdr_dev* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+int otdr_dev_kernels_per_iteration(const otdr_dev* ctx) {
+  (void)ctx;
+  return 3;
+}
+
+otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
+  if (!cfg || !out) return OTDR_E_INVALID_ARG;
+  *out = nullptr;
+  if (cfg->m < 1 || cfg->n < 1) return OTDR_E_DIMENSION;
+  const int nranks = cfg->nranks < 1 ? 1 : cfg->nranks;
+  if (cfg->row_begin < 0 || cfg->row_end > cfg->m || cfg->row_begin > cfg->row_end)
+    return OTDR_E_DIMENSION;
+  if (nranks == 1 && (cfg->row_begin != 0 || cfg->row_end != cfg->m)) return OTDR_E_DIMENSION;
+  if (nranks > 1 && !cfg->nccl_id) return OTDR_E_INVALID_ARG;
+  if (!otdr_dev_cuda_available()) return OTDR_E_CUDA;
+  otdr_dev* ctx = new otdr_dev();
+  ctx->cfg = *cfg;
+  ctx->cfg.nranks = nranks;
+  ctx->cfg.nccl_id = nullptr;
+  try {
+    CK(cudaSetDevice(cfg->device));
+    ctx->storage = cfg->storage == OTDR_STORE_F64 ? OTDR_STORE_F64 : OTDR_STORE_F32;
+    ctx->esz = ctx->f64() ? 8 : 4;
+    ctx->m_glob = cfg->m;
+    ctx->n = cfg->n;
+    ctx->row0 = cfg->row_begin;
+    ctx->m_loc = cfg->row_end - cfg->row_begin;
+    const long long vec = ctx->f64() ? 2 : 4;
+    ctx->ld = (ctx->n + vec - 1) / vec * vec;
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&ctx->ev0));
+    CK(cudaEventCreate(&ctx->ev1));
+    const size_t mat = size_t(std::max<long long>(ctx->m_loc, 1)) * size_t(ctx->ld) * ctx->esz;
+    CK(cudaMalloc(&ctx->C, mat));
+    CK(cudaMalloc(&ctx->X, mat));
+    CK(cudaMemset(ctx->C, 0, mat));
+    CK(cudaMemset(ctx->X, 0, mat));
+    const size_t ml = size_t(std::max<long long>(ctx->m_loc, 1));
+    ctx->p = dalloc<double>(ml);
+    ctx->phi = dalloc<double>(ml);
+    ctx->a = dalloc<double>(ml);
+    ctx->r = dalloc<double>(ml);
+    ctx->q = dalloc<double>(size_t(ctx->ld));
+    ctx->psi = dalloc<double>(size_t(ctx->ld));
+    ctx->b = dalloc<double>(size_t(ctx->ld));
+    ctx->s = dalloc<double>(size_t(ctx->ld));
+    CK(cudaMemset(ctx->q, 0, size_t(ctx->ld) * 8));
+    CK(cudaMemset(ctx->b, 0, size_t(ctx->ld) * 8));
+    CK(cudaMemset(ctx->s, 0, size_t(ctx->ld) * 8));
+    ctx->exch = dalloc<double>(size_t(ctx->n) + 3);
+    ctx->plan_geometry();
+    ctx->bpart = dalloc<double>(size_t(ctx->RB + ctx->CB) * 3);
+    ctx->csum = dalloc<double>(otdrk::kCertVals);
+    const size_t stage_elems = std::min(kStageDoubles, ml * size_t(ctx->n));
+    ctx->stage = dalloc<double>(std::max<size_t>(stage_elems, size_t(ctx->n)));
+    ctx->d_dev_row = dalloc<long long>(ml);
+    ctx->dev_row.resize(size_t(ctx->m_loc));
+    std::iota(ctx->dev_row.begin(), ctx->dev_row.end(), 0LL);
+    CK(cudaMemcpy(ctx->d_dev_row, ctx->dev_row.data(), size_t(ctx->m_loc) * 8,
+                  cudaMemcpyHostToDevice));
+    ctx->d_prm = dalloc<Params>(1);
+    ctx->d_ctl = dalloc<Ctl>(1);
+    ctx->d_mx = dalloc<unsigned long long>(1);
+    CK(cudaMallocHost(&ctx->h_ctl, sizeof(Ctl)));
+    std::memset(ctx->h_ctl, 0, sizeof(Ctl));
+    CK(cudaMemset(ctx->d_ctl, 0, sizeof(Ctl)));
+    ctx->prm = Params{};
+    ctx->set_rho_params(2.0 / double(ctx->m_glob + ctx->n));
+    ctx->push_prm();
+    // psi padding: -inf keeps padded columns exactly 0 through the clamp.
+    std::vector<double> pad(size_t(ctx->ld), -std::numeric_limits<double>::infinity());
+    CK(cudaMemcpy(ctx->psi, pad.data(), size_t(ctx->ld) * 8, cudaMemcpyHostToDevice));
+    ctx->build_segments();
+    if (nranks > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, cfg->nccl_id, sizeof(id));
+      NK(ncclCommInitRank(&ctx->comm, nranks, id, cfg->rank));
+    }
+  } catch (const Error& e) {
+    ctx->release();
+    delete ctx;
+    return e.code;
+  }
+  *out = ctx;
+  return OTDR_OK;
+}
+
+void otdr_dev_destroy(otdr_dev* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->cfg.device);
+  ctx->release();
+  delete ctx;
+}
+
+otdr_status otdr_dev_set_problem(otdr_dev* ctx, const double* cost_rm, const double* p,
+                                 const double* q) {
+  if (!ctx) return OTDR_E_INVALID_ARG;
+  if (!cost_rm || !p || !q) return fail(ctx, OTDR_E_INVALID_ARG, "null problem buffer");
+  return guarded(ctx, [&] {
+    ctx->h_p.assign(p, p + ctx->m_loc);
+    ctx->h_q.assign(q, q + ctx->n);
+    if (ctx->f64()) ctx->upload_rows<double>((double*)ctx->C, cost_rm);
+    else ctx->upload_rows<float>((float*)ctx->C, cost_rm);
+    ctx->upload_vec_rows(ctx->p, p);
+    CK(cudaMemcpy(ctx->q, q, size_t(ctx->n) * 8, cudaMemcpyHostToDevice));
+    ctx->has_problem = true;
+    ctx->has_state = false;
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_build_sqdist_cost(otdr_dev* ctx, const double* src_pts,
+                                       const double* tgt_pts, int d, const double* p,
+                                       const double* q, int* all_zero) {
+  if (!ctx) return OTDR_E_INVALID_ARG;
+  if (!src_pts || !tgt_pts || !p || !q || d < 1)
+    return fail(ctx, OTDR_E_INVALID_ARG, "bad point cloud arguments");
+  return guarded(ctx, [&] {
+    // Source points in device row order.
+    std::vector<double> src(size_t(std::max<long long>(ctx->m_loc, 1)) * d);
+    for (long long h = 0; h < ctx->m_loc; ++h)
+      std::memcpy(&src[size_t(ctx->dev_row[h]) * d], src_pts + h * d, sizeof(double) * d);
+    double* d_src = dalloc<double>(src.size());
+    double* d_tgt = dalloc<double>(size_t(ctx->n) * d);
+    double* d_mxv = dalloc<double>(1);
+    CK(cudaMemcpy(d_src, src.data(), src.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_tgt, tgt_pts, size_t(ctx->n) * d * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemsetAsync(ctx->d_mx, 0, 8, ctx->stream));
+    const int grid = 8 * kNumSMs;
+    if (ctx->f64())
+      otdrk::sqdist_kernel<double><<<grid, 256, 0, ctx->stream>>>((double*)ctx->C, d_src, d_tgt, d, ctx->m_loc, ctx->n, ctx->ld, d_mxv, ctx->d_mx, 0);
+    else
+      otdrk::sqdist_kernel<float><<<grid, 256, 0, ctx->stream>>>((float*)ctx->C, d_src, d_tgt, d, ctx->m_loc, ctx->n, ctx->ld, d_mxv, ctx->d_mx, 0);
+    ctx->check_launch();
+    CK(cudaMemcpyAsync(d_mxv, ctx->d_mx, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (ctx->comm) NK(ncclAllReduce(d_mxv, d_mxv, 1, ncclDouble, ncclMax, ctx->comm, ctx->stream));
+    if (ctx->f64())
+      otdrk::sqdist_kernel<double><<<grid, 256, 0, ctx->stream>>>((double*)ctx->C, d_src, d_tgt, d, ctx->m_loc, ctx->n, ctx->ld, d_mxv, ctx->d_mx, 1);
+    else
+      otdrk::sqdist_kernel<float><<<grid, 256, 0, ctx->stream>>>((float*)ctx->C, d_src, d_tgt, d, ctx->m_loc, ctx->n, ctx->ld, d_mxv, ctx->d_mx, 1);
+    ctx->check_launch();
+    double mx = 0.0;
+    CK(cudaMemcpyAsync(&mx, d_mxv, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_src);
+    cudaFree(d_tgt);
+    cudaFree(d_mxv);
+    if (all_zero) *all_zero = mx > 0.0 ? 0 : 1;
+    ctx->h_p.assign(p, p + ctx->m_loc);
+    ctx->h_q.assign(q, q + ctx->n);
+    ctx->upload_vec_rows(ctx->p, p);
+    CK(cudaMemcpy(ctx->q, q, size_t(ctx->n) * 8, cudaMemcpyHostToDevice));
+    ctx->has_problem = true;
+    ctx->has_state = false;
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_set_regularizer(otdr_dev* ctx, otdr_reg_kind kind, double param,
+                                     const int32_t* row_labels) {
+  if (!ctx) return OTDR_E_INVALID_ARG;
+  if (kind == OTDR_REG_QUAD && !(param > 0.0 && std::isfinite(param)))
+    return fail(ctx, OTDR_E_INVALID_ARG, "quadratic regularizer needs alpha > 0");
+  if (kind == OTDR_REG_GROUP_LASSO && !(param > 0.0 && std::isfinite(param)))
+    return fail(ctx, OTDR_E_INVALID_ARG, "group lasso needs lambda > 0");
+  if (kind != OTDR_REG_NONE && kind != OTDR_REG_QUAD && kind != OTDR_REG_GROUP_LASSO)
+    return fail(ctx, OTDR_E_UNSUPPORTED, "unsupported regularizer kind");
+  if (kind == OTDR_REG_GROUP_LASSO && !row_labels && ctx->m_loc > 0)
+    return fail(ctx, OTDR_E_INVALID_ARG, "group lasso needs row labels");
+  return guarded(ctx, [&] {
+    std::vector<long long> order(size_t(ctx->m_loc));
+    std::iota(order.begin(), order.end(), 0LL);
+    if (kind == OTDR_REG_GROUP_LASSO) {
+      ctx->labels.assign(row_labels, row_labels + ctx->m_loc);
+      for (int32_t l : ctx->labels)
+        if (l < -1) return fail(ctx, OTDR_E_INVALID_ARG, "row labels must be >= -1");
+      // Stable class sort: grouped classes ascending, ungrouped (-1) rows last.
+      auto key = [&](long long h) {
+        const int32_t l = ctx->labels[size_t(h)];
+        return l < 0 ? std::numeric_limits<int64_t>::max() : int64_t(l);
+      };
+      std::stable_sort(order.begin(), order.end(),
+                       [&](long long x, long long y) { return key(x) < key(y); });
+    } else {
+      ctx->labels.clear();
+    }
+    std::vector<long long> new_row(size_t(ctx->m_loc));
+    for (long long d = 0; d < ctx->m_loc; ++d) new_row[size_t(order[size_t(d)])] = d;
+    ctx->reg_kind = kind;
+    ctx->reg_param = param;
+    ctx->permute_rows(new_row);
+    ctx->build_segments();
+    ctx->invalidate_graphs();
+    ctx->set_rho_params(ctx->prm.rho);
+    ctx->push_prm();
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_set_state(otdr_dev* ctx, const double* X0, const double* phi0,
+                               const double* psi0) {
+  if (!ctx) return OTDR_E_INVALID_ARG;
+  if (!ctx->has_problem) return fail(ctx, OTDR_E_STATE, "set_state before set_problem");
+  const bool warm = X0 || phi0 || psi0;
+  if (warm && !(X0 && phi0 && psi0))
+    return fail(ctx, OTDR_E_DIMENSION, "warm start dimensions do not match the problem");
+  return guarded(ctx, [&] {
+    if (warm) {
+      const size_t cnt = size_t(ctx->m_loc) * size_t(ctx->n);
+      for (size_t t = 0; t < cnt; ++t)
+        if (!std::isfinite(X0[t]) || X0[t] < 0.0)
+          return fail(ctx, OTDR_E_NEGATIVE, "warm-start plan must be finite and >= 0");
+      if (ctx->f64()) ctx->upload_rows<double>((double*)ctx->X, X0);
+      else ctx->upload_rows<float>((float*)ctx->X, X0);
+      ctx->upload_vec_rows(ctx->phi, phi0);
+      CK(cudaMemcpy(ctx->psi, psi0, size_t(ctx->n) * 8, cudaMemcpyHostToDevice));
+    } else {  // default_init (solver.cpp:59-66)
+      CK(cudaMemset(ctx->X, 0, size_t(std::max<long long>(ctx->m_loc, 1)) * ctx->ld * ctx->esz));
+      const double mn = double(ctx->m_glob + ctx->n);
+      const double ph = (1.0 + double(ctx->m_glob) / mn) / (3.0 * mn);
+      const double ps = (1.0 + double(ctx->n) / mn) / (3.0 * mn);
+      std::vector<double> vphi(size_t(std::max<long long>(ctx->m_loc, 1)), ph);
+      std::vector<double> vpsi(size_t(ctx->n), ps);
+      CK(cudaMemcpy(ctx->phi, vphi.data(), size_t(ctx->m_loc) * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(ctx->psi, vpsi.data(), size_t(ctx->n) * 8, cudaMemcpyHostToDevice));
+    }
+    ctx->seed_state();
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_load_state(otdr_dev* ctx, const double* X, const double* phi,
+                                const double* psi, const double* a, const double* b,
+                                const double* r, const double* s, double theta, double eta,
+                                int64_t k) {
+  if (!ctx) return OTDR_E_INVALID_ARG;
+  if (!ctx->has_problem) return fail(ctx, OTDR_E_STATE, "load_state before set_problem");
+  if (!X || !phi || !psi || !a || !b || !r || !s)
+    return fail(ctx, OTDR_E_INVALID_ARG, "load_state needs every state buffer");
+  return guarded(ctx, [&] {
+    if (ctx->f64()) ctx->upload_rows<double>((double*)ctx->X, X);
+    else ctx->upload_rows<float>((float*)ctx->X, X);
+    ctx->upload_vec_rows(ctx->phi, phi);
+    ctx->upload_vec_rows(ctx->a, a);
+    ctx->upload_vec_rows(ctx->r, r);
+    CK(cudaMemcpy(ctx->psi, psi, size_t(ctx->n) * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->b, b, size_t(ctx->n) * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->s, s, size_t(ctx->n) * 8, cudaMemcpyHostToDevice));
+    std::memset(ctx->h_ctl, 0, sizeof(Ctl));
+    ctx->h_ctl->theta[0] = ctx->h_ctl->theta[1] = theta;
+    ctx->h_ctl->eta = eta;
+    ctx->h_ctl->k = k;
+    ctx->push_ctl();
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->has_state = true;
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_step(otdr_dev* ctx, double rho, int64_t iters) {
+  if (!ctx) return OTDR_E_INVALID_ARG;
+  if (!ctx->has_state) return fail(ctx, OTDR_E_STATE, "step before set_state");
+  if (iters < 0) return fail(ctx, OTDR_E_INVALID_ARG, "iters must be >= 0");
+  return guarded(ctx, [&] {
+    ctx->pull_ctl();
+    ctx->h_ctl->done = 0;
+    ctx->h_ctl->fused_shifted = 0;
+    ctx->push_ctl();
+    ctx->set_rho_params(rho);
+    ctx->prm.solving = 0;
+    ctx->prm.fused = 0;
+    ctx->prm.record_trace = 0;
+    ctx->push_prm();
+    ctx->run_raw(iters);
+    CK(cudaStreamSynchronize(ctx->stream));
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_time_steps(otdr_dev* ctx, double rho, int64_t iters, double* ms) {
+  if (!ctx || !ms) return OTDR_E_INVALID_ARG;
+  if (!ctx->has_state) return fail(ctx, OTDR_E_STATE, "time_steps before set_state");
+  return guarded(ctx, [&] {
+    ctx->pull_ctl();
+    ctx->h_ctl->done = 0;
+    ctx->h_ctl->fused_shifted = 0;
+    ctx->push_ctl();
+    ctx->set_rho_params(rho);
+    ctx->prm.solving = 0;
+    ctx->prm.fused = 0;
+    ctx->prm.record_trace = 0;
+    ctx->push_prm();
+    if (iters >= 16) ctx->get_graph(0, 16, false, false);  // instantiate outside the timing
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaEventRecord(ctx->ev0, ctx->stream));
+    ctx->run_raw(iters);
+    CK(cudaEventRecord(ctx->ev1, ctx->stream));
+    CK(cudaEventSynchronize(ctx->ev1));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, ctx->ev0, ctx->ev1));
+    *ms = t;
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_profile(otdr_dev* ctx, double rho, int64_t iters, otdr_kernel_times* out) {
+  if (!ctx || !out) return OTDR_E_INVALID_ARG;
+  if (!ctx->has_state) return fail(ctx, OTDR_E_STATE, "profile before set_state");
+  return guarded(ctx, [&] {
+    ctx->pull_ctl();
+    ctx->h_ctl->done = 0;
+    ctx->h_ctl->fused_shifted = 0;
+    ctx->push_ctl();
+    ctx->set_rho_params(rho);
+    ctx->prm.solving = 0;
+    ctx->prm.fused = 0;
+    ctx->prm.record_trace = 0;
+    ctx->push_prm();
+    cudaEvent_t ev[5];
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    double acc[4] = {0, 0, 0, 0};
+    for (int64_t t = 0; t < iters; ++t) {
+      CK(cudaEventRecord(ev[0], ctx->stream));
+      ctx->launch_sweep(false, false);
+      CK(cudaEventRecord(ev[1], ctx->stream));
+      ctx->launch_reduce(false);
+      CK(cudaEventRecord(ev[2], ctx->stream));
+      ctx->launch_exchange(ctx->exch, size_t(ctx->n) + 3);
+      CK(cudaEventRecord(ev[3], ctx->stream));
+      ctx->launch_update(0, 0, 0);
+      CK(cudaEventRecord(ev[4], ctx->stream));
+      ctx->check_launch();
+      CK(cudaEventSynchronize(ev[4]));
+      for (int k = 0; k < 4; ++k) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+        acc[k] += ms;
+      }
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    const double it = double(std::max<int64_t>(iters, 1));
+    out->sweep_ms = acc[0] / it;
+    out->reduce_ms = acc[1] / it;
+    out->exchange_ms = acc[2] / it;
+    out->update_ms = acc[3] / it;
+    out->iterations = iters;
+    out->sweep_bytes = double(ctx->m_loc) * double(ctx->n) * 3.0 * double(ctx->esz);
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_solve(otdr_dev* ctx, const otdr_solve_opts* o, otdr_solve_result* res) {
+  if (!ctx || !o || !res) return OTDR_E_INVALID_ARG;
+  if (o->max_iter <= 0)
+    return fail(ctx, OTDR_E_ZERO_ITERS,
+                "max_iter must be positive, got " + std::to_string((long long)o->max_iter));
+  if (o->check_every <= 0) return fail(ctx, OTDR_E_INVALID_ARG, "check_every must be positive");
+  if (!(o->tol_primal > 0.0)) return fail(ctx, OTDR_E_INVALID_ARG, "tol_primal must be positive");
+  if (o->has_tol_gap && !(o->tol_gap > 0.0))
+    return fail(ctx, OTDR_E_INVALID_ARG, "tol_gap must be positive when set");
+  if (!ctx->has_state) return fail(ctx, OTDR_E_STATE, "solve before set_state");
+  return guarded(ctx, [&] {
+    const double rho = o->rho > 0.0 ? o->rho : 2.0 / double(ctx->m_glob + ctx->n);
+    const bool track = o->record_trace != 0;
+    const bool cert = o->has_tol_gap || o->record_trace;
+    ctx->set_rho_params(rho);
+    ctx->prm.tol_primal = o->tol_primal;
+    ctx->prm.tol_gap = o->has_tol_gap ? o->tol_gap : 0.0;
+    ctx->prm.has_tol_gap = o->has_tol_gap ? 1 : 0;
+    ctx->prm.max_iter = o->max_iter;
+    ctx->prm.check_every = o->check_every;
+    ctx->prm.record_trace = track ? 1 : 0;
+    ctx->prm.deterministic = o->deterministic ? 1 : 0;
+    ctx->prm.fused = o->fused ? 1 : 0;
+    ctx->prm.solving = 1;
+    if (track) {
+      const long long cap = o->max_iter / o->check_every + 2;
+      if (cap > ctx->trace_cap) {
+        if (ctx->d_trace) cudaFree(ctx->d_trace);
+        ctx->d_trace = dalloc<otdrk::TraceRow>(size_t(cap));
+        ctx->trace_cap = cap;
+        ctx->invalidate_graphs();
+      }
+    }
+    ctx->prm.trace_cap = ctx->trace_cap;
+    ctx->push_prm();
+    ctx->pull_ctl();
+    Ctl& c = *ctx->h_ctl;
+    c.k0 = c.k;
+    c.done = 0;
+    c.termination = otdrk::TERM_MAXITER;
+    c.want_cert = 0;
+    c.fused_shifted = 0;
+    c.best = std::numeric_limits<double>::infinity();
+    c.last_improvement = 0;
+    c.supp_changed = 0;
+    c.supp_count = 0;
+    c.support_last_change = 0;
+    c.trace_len = 0;
+    c.cnt_reduce = c.cnt_update = c.cnt_cert = 0;
+    ctx->push_ctl();
+    // The support mask of X_0 (solver.cpp:133-143) is implicit: the tracking
+    // sweep compares each entry's old and new sign.
+    CK(cudaStreamSynchronize(ctx->stream));
+    const bool use_while = ctx->comm == nullptr;
+    const int body = 4;
+    cudaGraphExec_t ex = use_while ? ctx->get_graph(1, body, track, cert)
+                                   : ctx->get_graph(0, 8, track, cert);
+    CK(cudaEventRecord(ctx->ev0, ctx->stream));
+    otdrk::stamp_t0_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_ctl);
+    if (use_while) {
+      CK(cudaGraphLaunch(ex, ctx->stream));
+    } else {
+      for (;;) {
+        CK(cudaGraphLaunch(ex, ctx->stream));
+        ctx->pull_ctl();
+        if (ctx->h_ctl->done) break;
+      }
+    }
+    CK(cudaEventRecord(ctx->ev1, ctx->stream));
+    CK(cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    ctx->pull_ctl();
+    if (ctx->h_ctl->termination == otdrk::TERM_NONFINITE) {
+      const long long kk = ctx->h_ctl->k - ctx->h_ctl->k0;
+      return fail(ctx, OTDR_E_NONFINITE,
+                  "non-finite iterate at iteration " + std::to_string(kk) +
+                      " (check rho and regularizer parameters)");
+    }
+    // Materialise X after an even fused iteration, then the objective.
+    if (ctx->prm.fused && ctx->h_ctl->fused_shifted) {
+      const long long cnt = ctx->m_loc * ctx->ld;
+      if (ctx->f64())
+        otdrk::unshift_kernel<double><<<4 * kNumSMs, 256, 0, ctx->stream>>>((double*)ctx->X, (const double*)ctx->C, ctx->d_prm, cnt);
+      else
+        otdrk::unshift_kernel<float><<<4 * kNumSMs, 256, 0, ctx->stream>>>((float*)ctx->X, (const float*)ctx->C, ctx->d_prm, cnt);
+      ctx->check_launch();
+      ctx->h_ctl->fused_shifted = 0;
+      ctx->push_ctl();
+    }
+    ctx->launch_cert(1, 0, 0);
+    ctx->check_launch();
+    ctx->pull_ctl();
+    res->iterations = ctx->h_ctl->k;
+    res->termination = ctx->h_ctl->termination;
+    res->rho = rho;
+    res->r_primal = ctx->h_ctl->r_primal;
+    res->objective = ctx->h_ctl->objective;
+    res->support_last_change = track ? ctx->h_ctl->support_last_change : -1;
+    res->trace_rows = track ? ctx->h_ctl->trace_len : 0;
+    res->device_ms = ms;
+    ctx->prm.solving = 0;
+    ctx->prm.fused = 0;
+    ctx->push_prm();
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_get_state(otdr_dev* ctx, double* X, double* phi, double* psi, double* a,
+                               double* b, double* r, double* s, double* theta, double* eta,
+                               int64_t* k) {
+  if (!ctx) return OTDR_E_INVALID_ARG;
+  if (!ctx->has_state) return fail(ctx, OTDR_E_STATE, "get_state before set_state");
+  return guarded(ctx, [&] {
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (X) {
+      if (ctx->f64()) ctx->download_rows<double>(X, (const double*)ctx->X);
+      else ctx->download_rows<float>(X, (const float*)ctx->X);
+    }
+    if (phi) ctx->download_vec_rows(phi, ctx->phi);
+    if (a) ctx->download_vec_rows(a, ctx->a);
+    if (r) ctx->download_vec_rows(r, ctx->r);
+    if (psi) CK(cudaMemcpy(psi, ctx->psi, size_t(ctx->n) * 8, cudaMemcpyDeviceToHost));
+    if (b) CK(cudaMemcpy(b, ctx->b, size_t(ctx->n) * 8, cudaMemcpyDeviceToHost));
+    if (s) CK(cudaMemcpy(s, ctx->s, size_t(ctx->n) * 8, cudaMemcpyDeviceToHost));
+    ctx->pull_ctl();
+    if (theta) *theta = ctx->h_ctl->theta[ctx->h_ctl->k & 1];
+    if (eta) *eta = ctx->h_ctl->eta;
+    if (k) *k = ctx->h_ctl->k;
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_objective(otdr_dev* ctx, double* out) {
+  if (!ctx || !out) return OTDR_E_INVALID_ARG;
+  if (!ctx->has_state) return fail(ctx, OTDR_E_STATE, "objective before set_state");
+  return guarded(ctx, [&] {
+    ctx->launch_cert(1, 0, 0);
+    ctx->check_launch();
+    ctx->pull_ctl();
+    *out = ctx->h_ctl->objective;
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_duality_gap(otdr_dev* ctx, double rho, otdr_certificate* out) {
+  if (!ctx || !out) return OTDR_E_INVALID_ARG;
+  if (!ctx->has_state) return fail(ctx, OTDR_E_STATE, "duality_gap before set_state");
+  return guarded(ctx, [&] {
+    ctx->set_rho_params(rho);
+    ctx->prm.solving = 0;
+    ctx->prm.fused = 0;
+    ctx->prm.record_trace = 0;
+    ctx->prm.has_tol_gap = 0;
+    ctx->prm.check_every = 1;
+    ctx->prm.max_iter = std::numeric_limits<long long>::max();
+    ctx->push_prm();
+    ctx->pull_ctl();
+    ctx->h_ctl->want_cert = 1;
+    ctx->h_ctl->done = 0;
+    ctx->push_ctl();
+    ctx->launch_cert(0, 0, 0);
+    ctx->check_launch();
+    ctx->pull_ctl();
+    out->dual_value = ctx->h_ctl->dual_value;
+    out->gap = ctx->h_ctl->gap;
+    out->dual_residual = ctx->h_ctl->dres;
+    ctx->h_ctl->done = 0;
+    ctx->h_ctl->want_cert = 0;
+    ctx->push_ctl();
+    CK(cudaStreamSynchronize(ctx->stream));
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_get_trace(otdr_dev* ctx, otdr_trace_row* rows, int64_t cap, int64_t* count) {
+  if (!ctx) return OTDR_E_INVALID_ARG;
+  return guarded(ctx, [&] {
+    ctx->pull_ctl();
+    const long long have = std::min<long long>(ctx->h_ctl->trace_len, ctx->trace_cap);
+    if (count) *count = have;
+    const long long take = std::min<long long>(have, cap);
+    if (take > 0 && rows) {
+      static_assert(sizeof(otdrk::TraceRow) == sizeof(otdr_trace_row), "trace row layout");
+      CK(cudaMemcpy(rows, ctx->d_trace, size_t(take) * sizeof(otdr_trace_row),
+                    cudaMemcpyDeviceToHost));
+    }
+    return OTDR_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,371 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle.
+
+Gates (SURVEY §8(d) parity protocol; north-star tolerances):
+  * fp64 storage: X, phi, psi after k in {1, 10, 100} steps within 1e-12 relative
+    (max-norm) of the oracle -- element-wise arithmetic is the reference's, only
+    the order of the row/column sums differs.
+  * fp32 storage vs the oracle run on the fp32-rounded C: within 1e-5 relative.
+  * solve(): same iteration count and termination as the oracle, objective and
+    r_primal within 1e-6.
+Plus the reference's own solver KATs re-run through the GPU-backed API.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+otdr = pytest.importorskip("paper_2305_18483_b200")
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def oracle_reg(ora, kind, param, labels, n):
+    if kind == "none":
+        return ora.zero_reg()
+    if kind == "quad":
+        return ora.quad_reg(param)
+    offs, cells = ora.column_class_blocks(labels, n)
+    return ora.group_lasso_reg(param, offs, cells)
+
+
+def dev_reg(kind, param, labels, n):
+    if kind == "none":
+        return otdr.ZeroReg()
+    if kind == "quad":
+        return otdr.QuadraticReg(param)
+    return otdr.GroupLassoReg(param, otdr.column_class_blocks(labels, n))
+
+
+SHAPES = [(1, 1), (2, 2), (4, 5), (6, 7), (20, 20), (33, 257), (300, 517)]
+REGS = [("none", 0.0), ("quad", 0.7), ("gl", 0.02)]
+
+
+@pytest.mark.parametrize("m,n", SHAPES)
+@pytest.mark.parametrize("kind,param", REGS)
+def test_steps_fp64_match_oracle(ora, m, n, kind, param):
+    C, p, q, *_ = ora.gaussian_problem(m, n, 5 + m)
+    labels = [i % 3 for i in range(m)]
+    pr = ora.Problem(C, p, q)
+    oreg = oracle_reg(ora, kind, param, labels, n)
+    st = ora.make_state(pr)
+    eng = otdr.Engine(m, n, "f64")
+    eng.set_problem(C, p, q)
+    eng.set_regularizer(dev_reg(kind, param, labels, n))
+    eng.set_state()
+    rho = ora.default_stepsize(m, n)
+    done = 0
+    for k in (1, 10, 100):
+        for _ in range(k - done):
+            ora.step(st, pr, oreg, rho)
+        eng.step(rho, k - done)
+        done = k
+        g = eng.get_state()
+        assert g.k == st.k == k
+        assert rel(g.X, st.X) <= 1e-12, (k, rel(g.X, st.X))
+        assert rel(g.phi, st.phi) <= 1e-12
+        assert rel(g.psi, st.psi) <= 1e-12
+        assert rel(g.a, st.a) <= 1e-12 and rel(g.b, st.b) <= 1e-12
+        assert abs(g.theta - st.theta) <= 1e-12 * max(1.0, abs(st.theta))
+
+
+@pytest.mark.parametrize("m,n", [(6, 7), (300, 517), (1000, 1000)])
+@pytest.mark.parametrize("kind,param", REGS)
+def test_steps_fp32_match_oracle(ora, m, n, kind, param):
+    C, p, q, *_ = ora.gaussian_problem(m, n, 11)
+    C32 = C.astype(np.float32).astype(np.float64)  # same inputs on both sides
+    labels = [i % 4 for i in range(m)]
+    pr = ora.Problem(C32, p, q)
+    oreg = oracle_reg(ora, kind, param * (m + n) if kind == "quad" else param, labels, n)
+    st = ora.make_state(pr)
+    eng = otdr.Engine(m, n, "f32")
+    eng.set_problem(C, p, q)
+    eng.set_regularizer(dev_reg(kind, param * (m + n) if kind == "quad" else param, labels, n))
+    eng.set_state()
+    rho = ora.default_stepsize(m, n)
+    done = 0
+    for k in (1, 10, 100):
+        for _ in range(k - done):
+            ora.step(st, pr, oreg, rho)
+        eng.step(rho, k - done)
+        done = k
+        g = eng.get_state()
+        assert rel(g.X, st.X) <= 1e-5, (k, rel(g.X, st.X))
+        assert rel(g.phi, st.phi) <= 1e-5
+        assert rel(g.psi, st.psi) <= 1e-5
+
+
+def test_recurrence_matches_textbook_dr_on_gpu(ora):
+    """test_solver.cpp:75-116 through the device step (warm starts, 0.7 rho)."""
+    worst = 0.0
+    for seed in range(0, 50, 3):
+        rng = ora.Rng(1000 + seed)
+        m, n = 2 + seed % 5, 2 + (seed // 5) % 6
+        C, p, q = ora.random_problem(rng, m, n)
+        pr = ora.Problem(C, p, q)
+        rho = ora.default_stepsize(m, n) if seed % 2 == 0 else 0.7 * ora.default_stepsize(m, n)
+        labels = [i % 2 for i in range(m)]
+        for _ in range(m * n):
+            rng.uniform01()
+        for kind, param in (("none", 0.0), ("quad", 0.7), ("gl", 0.02)):
+            init = None
+            if seed % 3 == 0:
+                X0 = np.array([[0.3 * rng.uniform01() for _ in range(n)] for _ in range(m)])
+                phi0 = np.array([rng.uniform01() - 0.5 for _ in range(m)])
+                psi0 = np.array([rng.uniform01() - 0.5 for _ in range(n)])
+                init = (X0, phi0, psi0)
+            ost = ora.make_state(pr, init)
+            xs, ys = ora.dr_reference(pr, oracle_reg(ora, kind, param, labels, n), rho,
+                                      ost.shadow(), 100)
+            eng = otdr.Engine(m, n, "f64")
+            eng.set_problem(C, p, q)
+            eng.set_regularizer(dev_reg(kind, param, labels, n))
+            eng.set_state(None if init is None else otdr.WarmStart(*init))
+            for t in range(100):
+                eng.step(rho, 1)
+                g = eng.get_state()
+                shadow = g.X + g.phi[:, None] + g.psi[None, :]
+                worst = max(worst, np.abs(g.X - xs[t]).max(), np.abs(shadow - ys[t]).max())
+    assert worst <= 1e-9
+
+
+def _both_solve(ora, C, p, q, kind, param, labels, storage="f64", **kw):
+    m, n = C.shape
+    Co = C if storage == "f64" else C.astype(np.float32).astype(np.float64)
+    orep = ora.solve(ora.Problem(Co, p, q), oracle_reg(ora, kind, param, labels, n), **kw)
+    init = kw.pop("init", None)
+    opts = otdr.SolverOptions(storage=storage, **{k: v for k, v in kw.items()})
+    if init is not None:
+        opts.init = otdr.WarmStart(*init)
+    drep = otdr.solve(otdr.Problem(C, p, q), dev_reg(kind, param, labels, n), opts)
+    return orep, drep
+
+
+@pytest.mark.parametrize("kind,param", [("none", 0.0), ("quad", 0.05), ("gl", 0.01)])
+def test_solve_matches_oracle_small(ora, kind, param):  # test_solver.cpp:393-412
+    rng = ora.Rng(29)
+    C, p, q = ora.random_problem(rng, 20, 20)
+    labels = [i % 4 for i in range(20)]
+    orep, drep = _both_solve(ora, C, p, q, kind, param, labels, tol_primal=1e-6, max_iter=200000)
+    assert drep.termination.name == orep.termination == "Converged"
+    assert drep.iterations == orep.iterations
+    assert abs(drep.objective - orep.objective) <= 1e-6 * max(1.0, abs(orep.objective))
+    assert abs(drep.r_primal - orep.r_primal) <= 1e-6
+    assert rel(drep.plan(), orep.state.X) <= 1e-9
+
+
+def test_solve_gaussian_1000_quad(ora):
+    """cfg1: quadratic 1000^2, alpha = 5e-3 (m+n), tol 1e-4 -- both storages."""
+    C, p, q, *_ = ora.gaussian_problem(1000, 1000, 0)
+    for storage in ("f64", "f32"):
+        orep, drep = _both_solve(ora, C, p, q, "quad", 10.0, None, storage=storage, tol_primal=1e-4)
+        assert drep.termination.name == orep.termination == "Converged"
+        if storage == "f64":
+            assert drep.iterations == orep.iterations
+        else:
+            assert abs(drep.iterations - orep.iterations) <= max(2, orep.iterations // 100)
+        assert abs(drep.objective - orep.objective) <= 1e-6 * abs(orep.objective)
+        assert drep.r_primal <= 1e-4
+
+
+def test_2x2_diagonal_and_1x1(ora):  # test_solver.cpp:139-154, :170-192
+    pr = otdr.validate_problem([[0.0, 1.0], [1.0, 0.0]], [0.5, 0.5], [0.5, 0.5])
+    rep = otdr.solve(pr, otdr.ZeroReg(), otdr.SolverOptions(tol_primal=1e-8))
+    assert rep.termination == otdr.Termination.Converged
+    assert np.abs(rep.plan() - np.diag([0.5, 0.5])).max() <= 1e-6
+    assert abs(rep.objective) <= 1e-6
+    one = otdr.validate_problem([[0.8]], [1.0], [1.0])
+    for reg in (otdr.ZeroReg(), otdr.QuadraticReg(3.0),
+                otdr.GroupLassoReg(2.0, otdr.make_partition(1, 1, [[(0, 0)]]))):
+        rep = otdr.solve(one, reg, otdr.SolverOptions(tol_primal=1e-10, max_iter=200000))
+        assert rep.termination == otdr.Termination.Converged
+        assert abs(rep.plan()[0, 0] - 1.0) <= 1e-8
+
+
+def test_stall_window_gpu(ora):  # test_solver.cpp:272-286
+    rng = ora.Rng(17)
+    C, p, q = ora.random_problem(rng, 3, 3)
+    reg = otdr.GroupLassoReg(1e9, otdr.column_class_blocks([0, 0, 0], 3))
+    rep = otdr.solve(otdr.Problem(C, p, q), reg, otdr.SolverOptions(max_iter=30000))
+    assert rep.termination == otdr.Termination.Stalled
+    assert rep.iterations == 10001
+    assert rep.r_primal > 0.1
+
+
+def test_nonfinite_and_options(ora):  # test_solver.cpp:288-340
+    pr = otdr.validate_problem([[0.1, 0.9]], [1.0], [0.5, 0.5])
+    with pytest.raises(otdr.NonFiniteIterate, match="non-finite iterate at iteration 1"):
+        otdr.solve(pr, otdr.ZeroReg(), otdr.SolverOptions(
+            init=otdr.WarmStart(np.full((1, 2), 1e308), np.zeros(1), np.zeros(2))))
+    pr = otdr.validate_problem([[0.0, 1.0], [1.0, 0.0]], [0.5, 0.5], [0.5, 0.5])
+    z = otdr.ZeroReg()
+    with pytest.raises(otdr.ZeroIterations):
+        otdr.solve(pr, z, otdr.SolverOptions(max_iter=0))
+    with pytest.raises(ValueError):
+        otdr.solve(pr, z, otdr.SolverOptions(check_every=0))
+    with pytest.raises(ValueError):
+        otdr.solve(pr, z, otdr.SolverOptions(tol_primal=0.0))
+    with pytest.raises(ValueError):
+        otdr.solve(pr, z, otdr.SolverOptions(tol_gap=0.0))
+    with pytest.raises(otdr.DimensionMismatch):
+        otdr.solve(pr, z, otdr.SolverOptions(init=otdr.WarmStart(np.zeros((3, 2)), np.zeros(3), np.zeros(2))))
+    with pytest.raises(otdr.NegativeEntry):
+        otdr.solve(pr, z, otdr.SolverOptions(init=otdr.WarmStart(np.full((2, 2), -0.1), np.zeros(2), np.zeros(2))))
+
+
+@pytest.mark.parametrize("storage", ["f64", "f32"])
+def test_fused_matches_unfused(ora, storage):  # test_solver.cpp:342-357
+    rng = ora.Rng(19)
+    for _ in range(3):
+        C, p, q = ora.random_problem(rng, 4, 5)
+        pr = otdr.Problem(C, p, q)
+        a = otdr.solve(pr, otdr.QuadraticReg(0.4), otdr.SolverOptions(max_iter=501, tol_primal=1e-300, storage=storage))
+        b = otdr.solve(pr, otdr.QuadraticReg(0.4), otdr.SolverOptions(max_iter=501, tol_primal=1e-300, fused=True, storage=storage))
+        assert a.iterations == b.iterations == 501
+        tol = 1e-12 if storage == "f64" else 1e-5
+        assert rel(b.plan(), a.plan()) <= tol
+        assert rel(b.state.phi, a.state.phi) <= tol
+
+
+def test_trace_and_tol_gap(ora):  # test_solver.cpp:414-440, test_duality.cpp:99-108
+    rng = ora.Rng(41)
+    C, p, q = ora.random_problem(rng, 20, 20)
+    orep, drep = _both_solve(ora, C, p, q, "quad", 0.05, None, tol_primal=1e-7, max_iter=200000,
+                             record_trace=True, check_every=10, deterministic=True)
+    assert drep.termination.name == "Converged" and drep.iterations == orep.iterations
+    assert drep.support_last_change == orep.support_last_change
+    assert len(drep.trace) == len(orep.trace)
+    for dr, orow in zip(drep.trace, orep.trace):
+        assert dr.iter == orow[0] and dr.support == orow[4]
+        assert abs(dr.r_primal - orow[1]) <= 1e-9
+        assert abs(dr.gap - orow[2]) <= 1e-8 and abs(dr.dual_residual - orow[3]) <= 1e-8
+    pr = otdr.validate_problem([[0, 1], [1, 0]], [0.5, 0.5], [0.5, 0.5])
+    rep = otdr.solve(pr, otdr.ZeroReg(), otdr.SolverOptions(tol_primal=1e-8, tol_gap=1e-7, max_iter=500000))
+    o = ora.solve(ora.Problem(pr.cost, pr.p, pr.q), ora.zero_reg(), tol_primal=1e-8, tol_gap=1e-7, max_iter=500000)
+    assert rep.termination.name == o.termination == "Converged"
+    assert rep.iterations == o.iterations
+
+
+def test_certificate_1x1():  # test_duality.cpp:68-86
+    pr = otdr.validate_problem([[0.2]], [1.0], [1.0])
+    st = otdr.make_state(pr, otdr.WarmStart(np.ones((1, 1)), np.array([0.5]), np.array([0.25])))
+    cert = otdr.duality_gap(pr, otdr.ZeroReg(), st, 0.5)
+    assert cert.mu[0] == pytest.approx(1.0, rel=1e-15) and cert.nu[0] == pytest.approx(0.5, rel=1e-15)
+    assert cert.dual_value == pytest.approx(1.5, rel=1e-14)
+    assert cert.gap == pytest.approx(0.2 - 1.5, rel=1e-14)
+    assert cert.dual_residual == pytest.approx(0.65, rel=1e-14)
+
+
+@pytest.mark.parametrize("kind,param", REGS)
+def test_certificate_and_objective_match_oracle(ora, kind, param):
+    C, p, q, *_ = ora.gaussian_problem(37, 45, 3)
+    labels = [i % 3 for i in range(37)]
+    pr = ora.Problem(C, p, q)
+    st = ora.make_state(pr)
+    oreg = oracle_reg(ora, kind, param, labels, 45)
+    rho = ora.default_stepsize(37, 45)
+    for _ in range(30):
+        ora.step(st, pr, oreg, rho)
+    dv, gap, dres = ora.duality_gap(pr, oreg, st, rho)
+    dpr = otdr.Problem(C, p, q)
+    dst = otdr.SolverState(st.X.copy(), st.phi.copy(), st.psi.copy(), st.a.copy(), st.b.copy(),
+                           st.theta, st.r.copy(), st.s.copy(), st.eta, st.k)
+    cert = otdr.duality_gap(dpr, dev_reg(kind, param, labels, 45), dst, rho)
+    assert abs(cert.dual_value - dv) <= 1e-10 * max(1, abs(dv))
+    assert abs(cert.gap - gap) <= 1e-10 * max(1, abs(gap))
+    assert abs(cert.dual_residual - dres) <= 1e-10 * max(1, abs(dres))
+    obj = otdr.primal_objective(dpr, st.X, dev_reg(kind, param, labels, 45))
+    assert abs(obj - ora.primal_objective(pr, st.X, oreg)) <= 1e-12 * max(1, abs(obj))
+
+
+def test_step_api_matches_oracle(ora):
+    """make_state / step on host-visible states (value semantics)."""
+    rng = ora.Rng(11)
+    C, p, q = ora.random_problem(rng, 5, 4)
+    pr = otdr.Problem(C, p, q)
+    st = otdr.make_state(pr)
+    ost = ora.make_state(ora.Problem(C, p, q))
+    rho = otdr.default_stepsize(5, 4)
+    for _ in range(50):
+        otdr.step(st, pr, otdr.QuadraticReg(0.3), rho)
+        ora.step(ost, ora.Problem(C, p, q), ora.quad_reg(0.3), rho)
+        assert abs(st.r.sum() - st.s.sum()) <= 1e-10
+    assert st.k == 50 and rel(st.X, ost.X) <= 1e-12
+
+
+def test_gl_interleaved_and_uncovered_rows(ora):
+    """Interleaved class labels (the test zoo's i%2) and a partition leaving a
+    row uncovered map onto the class-sorted kernel exactly."""
+    m, n = 9, 11
+    C, p, q, *_ = ora.gaussian_problem(m, n, 8)
+    groups = []
+    rows_a = [0, 3, 6]
+    rows_b = [1, 4, 7, 8]
+    for j in range(n):
+        groups.append([(i, j) for i in rows_a])
+        groups.append([(i, j) for i in rows_b])
+    part = otdr.make_partition(m, n, groups)
+    offs = np.array([0] + list(np.cumsum([len(g) for g in groups])), dtype=np.int64)
+    cells = np.array([c for g in groups for c in g], dtype=np.int32)
+    oreg = ora.group_lasso_reg(0.004, offs, cells)
+    pr = ora.Problem(C, p, q)
+    st = ora.make_state(pr)
+    eng = otdr.Engine(m, n, "f64")
+    eng.set_problem(C, p, q)
+    eng.set_regularizer(otdr.GroupLassoReg(0.004, part))
+    eng.set_state()
+    rho = ora.default_stepsize(m, n)
+    for _ in range(40):
+        ora.step(st, pr, oreg, rho)
+    eng.step(rho, 40)
+    g = eng.get_state()
+    assert rel(g.X, st.X) <= 1e-12 and rel(g.phi, st.phi) <= 1e-12
+
+
+@pytest.mark.parametrize("storage", ["f64", "f32"])
+def test_device_cost_builder_matches_datagen(ora, storage):
+    m, n = 123, 77
+    C, p, q, src, tgt = ora.gaussian_problem(m, n, 9)
+    eng = otdr.Engine(m, n, storage)
+    zero = eng.build_sqdist_cost(src, tgt, p, q)
+    assert not zero
+    # the plan after one step from X = 0 exposes C through X1 = [phi+psi-rho C]_+
+    eng.set_regularizer(otdr.ZeroReg())
+    eng.set_state()
+    rho = 0.25
+    eng.step(rho, 1)
+    g = eng.get_state()
+    pr = ora.Problem(C if storage == "f64" else C.astype(np.float32).astype(np.float64), p, q)
+    st = ora.make_state(pr)
+    ora.step(st, pr, ora.zero_reg(), rho)
+    if storage == "f64":
+        assert np.array_equal(g.X, st.X)
+    else:
+        assert rel(g.X, st.X) <= 1e-6
+
+
+def test_large_fp32_properties(ora):
+    """Size-independent properties at 10000^2: mass balance sum r = sum s and
+    non-negativity after several sweeps (cfg2 shape)."""
+    m = n = 10000
+    _, p, q, src, tgt = ora.gaussian_problem(8, 8, 0)
+    rng = np.random.default_rng(0)
+    src = rng.normal(size=(m, 2))
+    tgt = rng.normal(size=(n, 2)) + 1.0
+    p = np.full(m, 1.0 / m)
+    q = np.full(n, 1.0 / n)
+    eng = otdr.Engine(m, n, "f32")
+    eng.build_sqdist_cost(src, tgt, p, q)
+    eng.set_regularizer(otdr.ZeroReg())
+    eng.set_state()
+    eng.step(otdr.default_stepsize(m, n), 20)
+    g = eng.get_state()
+    assert g.k == 20
+    assert (g.X >= 0).all()
+    assert abs(g.r.sum() - g.s.sum()) <= 1e-9
+    np.testing.assert_allclose(g.X.sum(axis=1) - p, g.r, atol=1e-9)
