@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""RDROT hot-path benchmark (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json north star, SURVEY §8(d) "headline n = 20000"):
+    gaussian_problem(20000, 20000, seed 0), QuadraticReg(alpha = 5e-3 (m+n) = 200),
+    rho = 2/(m+n), fp32 storage of C and X in HBM, fp64 arithmetic in registers.
+    One "step" = one full DR iteration over the 20000 x 20000 plan.
+    N > 1: the plan is row-sharded across N GPUs (one process per GPU) with one
+    NCCL all-reduce of the n+3 exchange vector per iteration -> strong scaling.
+
+value  : DR iterations/s with C and X resident in HBM (device time, CUDA events,
+         max over ranks). Inputs (3.2 GB) exceed the 126 MB L2, so no flush.
+e2e    : the same metric through the public API (otdr.solve on a host fp64
+         Problem in pinned memory): cost upload, the device solve, and the plan
+         download are all inside the timed region.
+roofline: the sweep kernel (12 B / plan entry / iteration) against the measured
+         HBM copy bandwidth of MEASURED_PEAKS.json.
+cpu_baseline: the CPU oracle (oracle/, a restatement of the reference solver;
+         the reference itself needs Eigen, absent here) on the host cores.
+
+`--impl reference` times that CPU restatement alone on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M = N = 20000
+SEED = 0
+ALPHA = 5e-3 * (M + N)
+WORKLOAD = "gaussian_problem(20000,20000,0) quadratic alpha=5e-3*(m+n)=200, fp32 C/X storage"
+METRIC = "DR iterations/s (20000x20000 quadratic RDROT)"
+UNIT = "iterations/s"
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the sweep from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        if d.get("workload") == WORKLOAD:
+            return d.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [ln.split(",") for ln in open(self.path).read().strip().splitlines() if ln.strip()]
+        except Exception:
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and "Active" in r[5 + k] and "Not" not in r[5 + k]:
+                    reasons.add(nm)
+        loaded = [s for s in sm if smax and s > 0.5 * max(smax)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def shard_rows(rank, world):
+    lo = M * rank // world
+    hi = M * (rank + 1) // world
+    return lo, hi
+
+
+def init_dist(world, local_rank):
+    if world <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    return dist
+
+
+def max_over_ranks(dist, value: float) -> float:
+    if dist is None:
+        return value
+    import torch
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def bcast_nccl_id(dist, rank):
+    from paper_2305_18483_b200 import _native as nat
+
+    buf = bytearray(128)
+    if rank == 0:
+        import ctypes as ct
+
+        raw = ct.create_string_buffer(128)
+        rc = nat.lib().otdr_dev_nccl_unique_id(raw)
+        if rc:
+            raise RuntimeError("ncclGetUniqueId failed")
+        buf = bytearray(raw.raw)
+    obj = [bytes(buf)]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def make_engine(rank, world, dist, local_rank):
+    import paper_2305_18483_b200 as otdr
+    from paper_2305_18483_b200 import datagen
+
+    lo, hi = shard_rows(rank, world)
+    shard = None
+    if world > 1:
+        shard = otdr.Shard(rank, world, lo, hi, bcast_nccl_id(dist, rank))
+    eng = otdr.Engine(M, N, "f32", device=local_rank if world > 1 else 0, shard=shard)
+    src, tgt = datagen.gaussian_points(M, N, SEED)
+    eng.build_sqdist_cost(src[lo:hi], tgt, datagen.uniform(M)[lo:hi], datagen.uniform(N))
+    eng.set_regularizer(otdr.QuadraticReg(ALPHA))
+    eng.set_state()
+    return eng
+
+
+def cpu_oracle_rate(iters: int, threads: int):
+    """Times `iters` DR iterations of the oracle on the host; returns (it/s, s/it)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as ora
+
+    C, p, q, *_ = ora.gaussian_problem(M, N, SEED)
+    pr = ora.Problem(C, p, q)
+    st = ora.make_state(pr)
+    reg = ora.quad_reg(ALPHA)
+    rho = ora.default_stepsize(M, N)
+    ora.step(st, pr, reg, rho, threads=threads)  # warm (page-in)
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        ora.step(st, pr, reg, rho, threads=threads)
+    dt = time.perf_counter() - t0
+    return iters / dt, dt / iters
+
+
+def run_reference(args):
+    rank, local_rank, world = env_rank()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as ora
+
+    C, p, q, *_ = ora.gaussian_problem(M, N, SEED)
+    pr = ora.Problem(C, p, q)
+    st = ora.make_state(pr)
+    reg = ora.quad_reg(ALPHA)
+    rho = ora.default_stepsize(M, N)
+    for _ in range(args.warmup):
+        ora.step(st, pr, reg, rho, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ora.step(st, pr, reg, rho, threads=threads)
+    dt = time.perf_counter() - t0
+    value = args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded gaussian_problem)",
+        "config": {"workload": WORKLOAD.replace(", fp32 C/X storage", ", fp64 host (reference layout)"),
+                   "m": M, "n": N, "regularizer": "quadratic", "alpha": ALPHA},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} DR iterations of the full 20000x20000 instance, "
+                                   f"oracle/otdr_oracle.cpp with {threads} OpenMP threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference needs Eigen3 (absent): timed its C++ restatement oracle/otdr_oracle.cpp",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    rank, local_rank, world = env_rank()
+    dist = init_dist(world, local_rank)
+    import paper_2305_18483_b200 as otdr
+
+    eng = make_engine(rank, world, dist, local_rank)
+    rho = otdr.default_stepsize(M, N)
+    eng.step(rho, args.warmup)  # untimed warm-up iterations (graph instantiation inside)
+    eng.time_steps(rho, 0)
+    if dist:
+        dist.barrier()
+    import torch
+
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        ms = eng.time_steps(rho, args.steps)  # CUDA events on the context stream
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = max_over_ranks(dist, ms)
+    value = args.steps / (ms / 1e3)
+    clocks = clk.summary()
+
+    # roofline: the sweep kernel timed per launch with CUDA events
+    prof = eng.profile(rho, 10)
+    achieved = prof["sweep_bytes"] / (prof["sweep_ms"] * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+    traffic = ncu_traffic()
+
+    # time to tolerance (device-resident solve loop)
+    t_rep = eng.solve(otdr.SolverOptions(tol_primal=1e-4, max_iter=5000, storage="f32"),
+                      with_state=False)
+    tt = max_over_ranks(dist, t_rep.device_ms)
+
+    # e2e through the public API: host fp64 problem (pinned) -> solve -> plan back
+    e2e = e2e_measure(rank, world, dist, local_rank, args)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        rate, spi = cpu_oracle_rate(args.cpu_iters, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{args.cpu_iters} DR iterations of the full 20000x20000 instance "
+                         f"(oracle/otdr_oracle.cpp, {threads} OpenMP threads); time-to-1e-4 "
+                         f"extrapolated {t_rep.iterations * spi:.1f} s"}
+
+    if rank == 0:
+        kpi = eng.kernels_per_iteration()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded gaussian_problem, reference generator)",
+            "config": {"workload": WORKLOAD, "m": M, "n": N, "regularizer": "quadratic",
+                       "alpha": ALPHA, "rho": rho, "storage": "f32", "arithmetic": "f64",
+                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs (3.2 GB C+X) larger than the 126 MB L2; no flush"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "sweep (fused clamp+prox+row/col partial sums)",
+                         "bytes_per_launch": prof["sweep_bytes"], "sweep_ms": prof["sweep_ms"],
+                         "reduce_ms": prof["reduce_ms"], "exchange_ms": prof["exchange_ms"],
+                         "update_ms": prof["update_ms"], "peak_source": peak_src},
+            "time_to_tol": {"tol_primal": 1e-4, "iterations": t_rep.iterations,
+                            "termination": t_rep.termination.name, "device_s": tt / 1e3},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": args.steps * kpi,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_measure(rank, world, dist, local_rank, args):
+    """One public-API solve per step on a host fp64 Problem in pinned memory."""
+    import torch
+
+    import paper_2305_18483_b200 as otdr
+    from paper_2305_18483_b200 import datagen
+
+    lo, hi = shard_rows(rank, world)
+    src, tgt = datagen.gaussian_points(M, N, SEED)
+    host = torch.empty((hi - lo, N), dtype=torch.float64, pin_memory=torch.cuda.is_available())
+    C = host.numpy()
+    # cost rows of the global normalize_cost(squared_distance_cost) (datagen.cpp:56-65)
+    mx = 0.0
+    for r0 in range(0, M, 2000):
+        mx = max(mx, float(datagen.squared_distance_cost(src[r0:r0 + 2000], tgt).max()))
+    for r0 in range(lo, hi, 2000):
+        r1 = min(hi, r0 + 2000)
+        C[r0 - lo:r1 - lo] = datagen.squared_distance_cost(src[r0:r1], tgt) / mx
+    p = datagen.uniform(M)[lo:hi].copy()
+    q = datagen.uniform(N)
+    plan_host = torch.empty((hi - lo, N), dtype=torch.float64, pin_memory=torch.cuda.is_available()).numpy()
+    shard = None
+    reg = otdr.QuadraticReg(ALPHA)
+    iters = args.e2e_iters
+    times = []
+    for rep in range(2):  # first call warms the allocator / graph instantiation
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        if world > 1:
+            shard = otdr.Shard(rank, world, lo, hi, bcast_nccl_id(dist, rank))
+        eng = otdr.Engine(M, N, "f32", device=local_rank if world > 1 else 0, shard=shard)
+        eng.set_problem(C, p, q)                      # H2D of the cost inside the timed region
+        eng.set_regularizer(reg)
+        eng.set_state()
+        r = eng.solve(otdr.SolverOptions(tol_primal=1e-300, max_iter=iters, storage="f32"),
+                      with_state=False)
+        eng.get_plan_into(plan_host)                  # D2H of the plan
+        dt = time.perf_counter() - t0
+        eng.close()
+        times.append(max_over_ranks(dist, dt))
+    dt = times[-1]
+    return {"value": iters / dt, "unit": UNIT, "h2d_bytes_per_step": 8 * (hi - lo) * N + 8 * (hi - lo + N),
+            "d2h_bytes_per_step": 8 * (hi - lo) * N,
+            "step": f"one public-API solve of {iters} DR iterations (Engine create, fp64 cost upload "
+                    f"from pinned host memory, device loop, plan download)",
+            "seconds_per_solve": dt, "iterations": int(r.iterations)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-iters", type=int, default=3)
+    ap.add_argument("--e2e-iters", type=int, default=350)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -67,6 +67,8 @@ EXPORTS = [
     "otdr_dev_solve", "otdr_dev_get_state", "otdr_dev_objective", "otdr_dev_duality_gap",
     "otdr_dev_get_trace", "otdr_dev_profile", "otdr_dev_time_steps",
     "otdr_dev_kernels_per_iteration",
+    # include/otdr_datagen.h
+    "otdr_gaussian_points", "otdr_adaptation_points", "otdr_dev_nccl_unique_id",
 ]
 
 _lib = None
@@ -104,6 +106,11 @@ def lib():
     L.otdr_dev_get_trace.argtypes = [vp, ct.POINTER(TraceRow), ct.c_int64, _i64p]
     L.otdr_dev_profile.argtypes = [vp, ct.c_double, ct.c_int64, ct.POINTER(KernelTimes)]
     L.otdr_dev_time_steps.argtypes = [vp, ct.c_double, ct.c_int64, _dp]
+    L.otdr_gaussian_points.argtypes = [ct.c_int64, ct.c_int64, ct.c_uint64, _dp, _dp]
+    L.otdr_gaussian_points.restype = None
+    L.otdr_adaptation_points.argtypes = [ct.c_int64, ct.c_int64, ct.c_int, ct.c_uint64, ct.c_int,
+                                         _dp, _dp, _i32p, _i32p]
+    L.otdr_dev_nccl_unique_id.argtypes = [ct.c_char_p]
     L.otdr_dev_kernels_per_iteration.argtypes = [vp]
     L.otdr_dev_kernels_per_iteration.restype = ct.c_int
     _lib = L

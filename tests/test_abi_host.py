@@ -14,8 +14,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def declared_symbols():
-    src = open(os.path.join(ROOT, "include", "otdr_dev.h")).read()
-    return sorted(set(re.findall(r"\b(otdr_dev_\w+)\s*\(", src)))
+    names = set()
+    for hdr in ("otdr_dev.h", "otdr_datagen.h"):
+        src = open(os.path.join(ROOT, "include", hdr)).read()
+        names |= set(re.findall(r"^\S.*\b(otdr_\w+)\s*\(", src, flags=re.M))
+    return sorted(names)
 
 
 def test_library_exports_every_declared_symbol():
