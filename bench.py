@@ -36,6 +36,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+try:  # load torch (and its bundled NCCL) before libotdr_dev.so binds NCCL lazily
+    import torch  # noqa: F401
+except Exception:  # pragma: no cover - torch is plumbing only
+    torch = None
+
 M = N = 20000
 SEED = 0
 ALPHA = 5e-3 * (M + N)
@@ -275,7 +280,7 @@ def run_ours(args):
     tt = max_over_ranks(dist, t_rep.device_ms)
 
     # e2e through the public API: host fp64 problem (pinned) -> solve -> plan back
-    e2e = e2e_measure(rank, world, dist, local_rank, args)
+    e2e = None if args.no_e2e else e2e_measure(rank, world, dist, local_rank, args)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -376,6 +381,7 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=3)
     ap.add_argument("--e2e-iters", type=int, default=350)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

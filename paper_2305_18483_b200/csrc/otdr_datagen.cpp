@@ -4,8 +4,6 @@
 // reference's baseline-x86-64 build.
 #include "otdr_datagen.h"
 
-#include <nccl.h>
-
 #include <cmath>
 #include <cstring>
 #include <random>
@@ -100,14 +98,6 @@ int otdr_adaptation_points(int64_t m, int64_t n, int classes, uint64_t seed, int
       tgt[2 * j + 1] = sa * x + ca * y + ty;
     }
   }
-  return 0;
-}
-
-int otdr_dev_nccl_unique_id(unsigned char* out128) {
-  ncclUniqueId id;
-  if (ncclGetUniqueId(&id) != ncclSuccess) return 9;
-  static_assert(sizeof(id) == 128, "ncclUniqueId size");
-  std::memcpy(out128, &id, sizeof(id));
   return 0;
 }
 

@@ -10,6 +10,7 @@
 #include "otdr_kernels.cuh"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -44,11 +45,43 @@ struct Error {
     if (e_ != cudaSuccess)                                                            \
       throw Error{OTDR_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)};   \
   } while (0)
+// NCCL is bound at run time (dlopen) so the process uses whichever libnccl is
+// already loaded (e.g. the one PyTorch bundles); only row-sharded contexts
+// need it.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.GetUniqueId && a.CommInitRank && a.AllReduce && a.CommDestroy && a.GetErrorString;
+    return a;
+  }();
+  return api;
+}
+
 #define NK(expr)                                                                      \
   do {                                                                                \
+    if (!nccl().ok) throw Error{OTDR_E_NCCL, "libnccl.so.2 could not be loaded"};     \
     ncclResult_t r_ = (expr);                                                         \
     if (r_ != ncclSuccess)                                                            \
-      throw Error{OTDR_E_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)};   \
+      throw Error{OTDR_E_NCCL, std::string(#expr) + ": " + nccl().GetErrorString(r_)}; \
   } while (0)
 
 template <typename T>
@@ -160,7 +193,7 @@ struct otdr_dev {
   }
 
   void launch_exchange(double* buf, size_t count) {
-    if (comm) NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, comm, stream));
+    if (comm) NK(nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, comm, stream));
   }
 
   void launch_update(cudaGraphConditionalHandle cond, int use_cond, int cert_follows) {
@@ -447,7 +480,7 @@ struct otdr_dev {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
-    if (comm) ncclCommDestroy(comm);
+    if (comm && nccl().ok) nccl().CommDestroy(comm);
   }
 };
 
@@ -473,6 +506,15 @@ otdr_status guarded(otdr_dev* ctx, F&& f) {
 }  // namespace
 
 extern "C" {
+
+int otdr_dev_nccl_unique_id(unsigned char* out128) {
+  if (!nccl().ok) return OTDR_E_NCCL;
+  ncclUniqueId id;
+  if (nccl().GetUniqueId(&id) != ncclSuccess) return OTDR_E_NCCL;
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, sizeof(id));
+  return OTDR_OK;
+}
 
 int otdr_dev_abi_version(void) { return OTDR_DEV_ABI_VERSION; }
 
@@ -559,7 +601,7 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     if (nranks > 1) {
       ncclUniqueId id;
       std::memcpy(&id, cfg->nccl_id, sizeof(id));
-      NK(ncclCommInitRank(&ctx->comm, nranks, id, cfg->rank));
+      NK(nccl().CommInitRank(&ctx->comm, nranks, id, cfg->rank));
     }
   } catch (const Error& e) {
     ctx->release();
@@ -618,7 +660,7 @@ otdr_status otdr_dev_build_sqdist_cost(otdr_dev* ctx, const double* src_pts,
       otdrk::sqdist_kernel<float><<<grid, 256, 0, ctx->stream>>>((float*)ctx->C, d_src, d_tgt, d, ctx->m_loc, ctx->n, ctx->ld, d_mxv, ctx->d_mx, 0);
     ctx->check_launch();
     CK(cudaMemcpyAsync(d_mxv, ctx->d_mx, 8, cudaMemcpyDeviceToDevice, ctx->stream));
-    if (ctx->comm) NK(ncclAllReduce(d_mxv, d_mxv, 1, ncclDouble, ncclMax, ctx->comm, ctx->stream));
+    if (ctx->comm) NK(nccl().AllReduce(d_mxv, d_mxv, 1, ncclDouble, ncclMax, ctx->comm, ctx->stream));
     if (ctx->f64())
       otdrk::sqdist_kernel<double><<<grid, 256, 0, ctx->stream>>>((double*)ctx->C, d_src, d_tgt, d, ctx->m_loc, ctx->n, ctx->ld, d_mxv, ctx->d_mx, 1);
     else

@@ -1,0 +1,472 @@
+// C++ API suite: the reference's test_solver.cpp / test_regularizers.cpp /
+// test_problem.cpp / test_duality.cpp cases re-run against the B200 backend
+// through include/otdr_b200/otdr.hpp (the reference's own API names).
+//
+//   test_cpp_api          all cases (needs a CUDA device)
+//   test_cpp_api --cpu    host-side cases + "no GPU -> DeviceError, no fallback"
+//
+// The textbook-DR meta-oracle comes from the CPU oracle (oracle/otdr_oracle.h,
+// test infrastructure). Exit code = number of failed checks.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "otdr_b200/otdr.hpp"
+#include "otdr_dev.h"
+#include "otdr_oracle.h"
+
+using namespace otdr;
+
+namespace {
+
+int failures = 0;
+int checks = 0;
+std::string current;
+
+#define CHECK(cond)                                                                        \
+  do {                                                                                     \
+    ++checks;                                                                              \
+    if (!(cond)) {                                                                         \
+      ++failures;                                                                          \
+      std::printf("  FAIL %s:%d [%s] %s\n", __FILE__, __LINE__, current.c_str(), #cond);   \
+    }                                                                                      \
+  } while (0)
+
+template <typename E, typename F>
+bool throws_as(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+struct Rng {  // rng.hpp through the oracle (same mt19937_64 stream)
+  void* h;
+  explicit Rng(uint64_t s) : h(ora_rng_new(s)) {}
+  ~Rng() { ora_rng_free(h); }
+  double uniform01() { return ora_rng_uniform01(h); }
+};
+
+Problem random_problem(Rng& rng, Index m, Index n) {  // test_solver.cpp:19-29
+  Matrix c(m, n);
+  for (Index i = 0; i < m; ++i)
+    for (Index j = 0; j < n; ++j) c(i, j) = rng.uniform01();
+  Vector p(m), q(n);
+  for (Index i = 0; i < m; ++i) p[i] = rng.uniform01() + 0.05;
+  for (Index j = 0; j < n; ++j) q[j] = rng.uniform01() + 0.05;
+  const double sp = p.sum(), sq = q.sum();
+  for (Index i = 0; i < m; ++i) p[i] /= sp;
+  for (Index j = 0; j < n; ++j) q[j] /= sq;
+  return validate_problem(c, p, q);
+}
+
+double max_abs_diff(const Matrix& a, const Matrix& b) {
+  double w = 0.0;
+  for (Index t = 0; t < a.size(); ++t) w = std::max(w, std::abs(a.data()[t] - b.data()[t]));
+  return w;
+}
+
+double norm(const Vector& v) {
+  double s = 0.0;
+  for (Index i = 0; i < v.size(); ++i) s += v[i] * v[i];
+  return std::sqrt(s);
+}
+
+Matrix shadow(const SolverState& st) {
+  Matrix y = st.X;
+  for (Index i = 0; i < y.rows(); ++i)
+    for (Index j = 0; j < y.cols(); ++j) y(i, j) += st.phi[i] + st.psi[j];
+  return y;
+}
+
+struct OracleReg {  // CSR groups for the oracle's group-lasso prox
+  ora_reg r{};
+  std::vector<int64_t> offs;
+  std::vector<int32_t> cells;
+};
+
+OracleReg oracle_reg(const Regularizer& reg, const GroupPartition* part) {
+  OracleReg o;
+  o.r.kind = reg.kind();
+  o.r.param = reg.param();
+  if (part) {
+    for (auto off : part->offsets) o.offs.push_back(static_cast<int64_t>(off));
+    for (auto [i, j] : part->cells) {
+      o.cells.push_back(i);
+      o.cells.push_back(j);
+    }
+    o.r.num_groups = static_cast<int64_t>(part->num_groups());
+    o.r.offsets = o.offs.data();
+    o.r.cells = o.cells.data();
+  }
+  return o;
+}
+
+void run(const char* name, const std::function<void()>& f) {
+  current = name;
+  const int before = failures;
+  try {
+    f();
+  } catch (const std::exception& e) {
+    ++failures;
+    std::printf("  FAIL [%s] unexpected exception: %s\n", name, e.what());
+  }
+  std::printf("%s %s\n", failures == before ? "PASS" : "FAIL", name);
+}
+
+// ----------------------------------------------------------- host-side cases
+void host_cases() {
+  run("default stepsize is 2/(m+n)", [] {  // test_solver.cpp:57-61
+    CHECK(std::abs(default_stepsize(2000, 3000) - 4e-4) <= 4e-4 * 1e-15);
+    CHECK(default_stepsize(1, 1) == 1.0);
+  });
+  run("default init: zero plan and pinned offsets", [] {  // test_solver.cpp:63-73
+    WarmStart w = default_init(2, 3);
+    CHECK(w.plan0.rows() == 2 && w.plan0.cols() == 3);
+    CHECK(std::abs(w.phi0[0] - 1.4 / 15.0) <= 1e-16);
+    CHECK(std::abs(w.psi0[0] - 1.6 / 15.0) <= 1e-16);
+  });
+  run("skip count: pinned values", [] {  // test_solver.cpp:194-212
+    Matrix c1(1, 1);
+    c1 << 1.0;
+    CHECK(compute_skip_count(validate_problem(c1, Vector::Ones(1), Vector::Ones(1)), 1.0) == 0);
+    const Index n = 100;
+    Problem big = validate_problem(Matrix::Ones(n, n), Vector::Constant(n, 1.0 / n),
+                                   Vector::Constant(n, 1.0 / n));
+    CHECK(compute_skip_count(big, default_stepsize(n, n)) == 16);
+  });
+  run("problem validation errors", [] {  // test_problem.cpp:42-78
+    Matrix c(2, 2);
+    c << 0, 1, 1, 0;
+    CHECK(throws_as<MarginalSumOutOfRange>([&] { validate_problem(c, Vector{0.5, 0.6}, Vector{0.5, 0.5}); }));
+    Matrix neg(2, 2);
+    neg << -1, 0, 0, 1;
+    CHECK(throws_as<NegativeEntry>([&] { validate_problem(neg, Vector{0.5, 0.5}, Vector{0.5, 0.5}); }));
+    CHECK(throws_as<DimensionMismatch>([&] { validate_problem(c, Vector::Constant(3, 1.0 / 3), Vector{0.5, 0.5}); }));
+    Problem pr = validate_problem(c, Vector{0.5 + 4e-7, 0.5}, Vector{0.5, 0.5 - 4e-7});
+    CHECK(std::abs(pr.p.sum() - 1.0) <= 1e-12);
+    Matrix c2(2, 2);
+    c2 << 2, 4, 1, 3;
+    Problem nrm = normalize_cost(validate_problem(c2, Vector{0.5, 0.5}, Vector{0.5, 0.5}));
+    Matrix want(2, 2);
+    want << 0.5, 1.0, 0.25, 0.75;
+    CHECK(nrm.cost == want);
+  });
+  run("groups: column_class_blocks order and validation", [] {  // test_groups.cpp
+    GroupPartition part = column_class_blocks({0, 1, 0, 1}, 3);
+    CHECK(part.num_groups() == 6);
+    CHECK((part.group(0)[1] == GroupPartition::Cell{2, 0}));
+    CHECK((part.group(1)[0] == GroupPartition::Cell{1, 0}));
+    CHECK(throws_as<std::invalid_argument>([] { column_class_blocks({0, -1}, 2); }));
+    CHECK(throws_as<std::invalid_argument>([] { make_partition(2, 2, {{{0, 0}, {0, 1}}, {{0, 1}}}); }));
+    GroupLassoReg ok(0.1, column_class_blocks({2, 0, 2, 1}, 3));
+    auto lab = ok.row_labels(4);
+    CHECK(lab[0] == lab[2] && lab[0] != lab[1] && lab[1] != lab[3]);
+    GroupLassoReg bad(0.1, make_partition(2, 2, {{{0, 0}, {0, 1}}}));
+    CHECK(throws_as<Unsupported>([&] { bad.row_labels(2); }));
+  });
+  run("option validation precedes the device", [] {  // test_solver.cpp:303-324
+    Matrix c(2, 2);
+    c << 0, 1, 1, 0;
+    Problem pr = validate_problem(c, Vector{0.5, 0.5}, Vector{0.5, 0.5});
+    SolverOptions bad;
+    bad.max_iter = 0;
+    CHECK(throws_as<ZeroIterations>([&] { solve(pr, ZeroReg(), bad); }));
+    SolverOptions ce;
+    ce.check_every = 0;
+    CHECK(throws_as<std::invalid_argument>([&] { solve(pr, ZeroReg(), ce); }));
+    SolverOptions tg;
+    tg.tol_gap = 0.0;
+    CHECK(throws_as<std::invalid_argument>([&] { solve(pr, ZeroReg(), tg); }));
+  });
+}
+
+void no_gpu_case() {
+  run("no CUDA device -> DeviceError (no CPU fallback)", [] {
+    Matrix c(2, 2);
+    c << 0, 1, 1, 0;
+    Problem pr = validate_problem(c, Vector{0.5, 0.5}, Vector{0.5, 0.5});
+    CHECK(throws_as<DeviceError>([&] { solve(pr, ZeroReg(), SolverOptions{}); }));
+  });
+}
+
+// ------------------------------------------------------------- device cases
+void device_cases() {
+  run("recurrence matches an exact-projection reference", [] {  // test_solver.cpp:75-116
+    double worst = 0.0;
+    for (int seed = 0; seed < 50; seed += 2) {
+      Rng rng(1000 + seed);
+      const Index m = 2 + seed % 5, n = 2 + (seed / 5) % 6;
+      Problem pr = random_problem(rng, m, n);
+      const double rho = (seed % 2 == 0) ? default_stepsize(m, n) : 0.7 * default_stepsize(m, n);
+      std::vector<int> labels(static_cast<std::size_t>(m));
+      for (Index i = 0; i < m; ++i) labels[static_cast<std::size_t>(i)] = static_cast<int>(i % 2);
+      for (Index t = 0; t < m * n; ++t) rng.uniform01();  // the zoo's WeightedL1 draws
+      GroupPartition part = column_class_blocks(labels, n);
+      std::vector<std::unique_ptr<Regularizer>> zoo;
+      zoo.emplace_back(new ZeroReg());
+      zoo.emplace_back(new QuadraticReg(0.7));
+      zoo.emplace_back(new GroupLassoReg(0.02, part));
+      for (std::size_t z = 0; z < zoo.size(); ++z) {
+        std::optional<WarmStart> init;
+        if (seed % 3 == 0) {
+          WarmStart w{Matrix(m, n), Vector(m), Vector(n)};
+          for (Index i = 0; i < m; ++i)
+            for (Index j = 0; j < n; ++j) w.plan0(i, j) = 0.3 * rng.uniform01();
+          for (Index i = 0; i < m; ++i) w.phi0[i] = rng.uniform01() - 0.5;
+          for (Index j = 0; j < n; ++j) w.psi0[j] = rng.uniform01() - 0.5;
+          init = w;
+        }
+        b200::Session sess(pr, *zoo[z]);
+        sess.set_state(init);
+        SolverState st = sess.state();
+        Matrix y0 = shadow(st);
+        OracleReg oreg = oracle_reg(*zoo[z], z == 2 ? &part : nullptr);
+        ora_problem op{m, n, pr.cost.data(), pr.p.data(), pr.q.data()};
+        std::vector<double> xs(static_cast<std::size_t>(100 * m * n)), ys(xs.size());
+        ora_dr_reference(&op, &oreg.r, rho, y0.data(), 100, xs.data(), ys.data());
+        for (int t = 0; t < 100; ++t) {
+          sess.step(rho, 1);
+          st = sess.state();
+          Matrix y = shadow(st);
+          for (Index e = 0; e < m * n; ++e) {
+            worst = std::max(worst, std::abs(st.X.data()[e] - xs[static_cast<std::size_t>(t * m * n + e)]));
+            worst = std::max(worst, std::abs(y.data()[e] - ys[static_cast<std::size_t>(t * m * n + e)]));
+          }
+        }
+      }
+    }
+    CHECK(worst <= 1e-9);
+  });
+  run("2x2 diagonal problem solves to the permutation plan", [] {  // :139-154
+    Matrix c(2, 2);
+    c << 0.0, 1.0, 1.0, 0.0;
+    Problem pr = validate_problem(c, Vector{0.5, 0.5}, Vector{0.5, 0.5});
+    SolverOptions opt;
+    opt.tol_primal = 1e-8;
+    SolveReport rep = solve(pr, ZeroReg(), opt);
+    CHECK(rep.termination == Termination::Converged);
+    Matrix want(2, 2);
+    want << 0.5, 0.0, 0.0, 0.5;
+    CHECK(max_abs_diff(rep.plan(), want) <= 1e-6);
+    CHECK(std::abs(rep.objective) <= 1e-6);
+  });
+  run("1x1 problems converge for any penalty", [] {  // :170-192
+    Matrix c(1, 1);
+    c << 0.8;
+    Problem pr = validate_problem(c, Vector::Ones(1), Vector::Ones(1));
+    std::vector<std::unique_ptr<Regularizer>> regs;
+    regs.emplace_back(new ZeroReg());
+    regs.emplace_back(new QuadraticReg(3.0));
+    regs.emplace_back(new GroupLassoReg(2.0, make_partition(1, 1, {{{0, 0}}})));
+    for (auto& reg : regs) {
+      SolverOptions opt;
+      opt.tol_primal = 1e-10;
+      opt.max_iter = 200000;
+      SolveReport rep = solve(pr, *reg, opt);
+      CHECK(rep.termination == Termination::Converged);
+      CHECK(std::abs(rep.plan()(0, 0) - 1.0) <= 1e-8);
+    }
+  });
+  run("skip count lower-bounds the zero run under the naive init", [] {  // :214-237
+    const Index n = 20;
+    Problem pr = validate_problem(Matrix::Ones(n, n), Vector::Constant(n, 1.0 / n),
+                                  Vector::Constant(n, 1.0 / n));
+    const double rho = default_stepsize(n, n);
+    WarmStart naive{Matrix(n, n), Vector::Zero(n), Vector::Zero(n)};
+    for (Index i = 0; i < n; ++i)
+      for (Index j = 0; j < n; ++j) naive.plan0(i, j) = pr.p[i] * pr.q[j];
+    SolverState st = make_state(pr, naive);
+    long zero_run = 0;
+    for (long k = 1; k <= 200; ++k) {
+      step(st, pr, ZeroReg(), rho);
+      bool all_zero = true;
+      for (Index t = 0; t < st.X.size(); ++t) all_zero = all_zero && st.X.data()[t] == 0.0;
+      if (all_zero) zero_run = k;
+      else break;
+    }
+    CHECK(zero_run == 19);
+    CHECK(compute_skip_count(pr, rho) <= zero_run);
+  });
+  run("row and column residuals carry the same total mass error", [] {  // :239-249
+    Rng rng(11);
+    Problem pr = random_problem(rng, 5, 4);
+    QuadraticReg quad(0.3);
+    b200::Session sess(pr, quad);
+    sess.set_state(std::nullopt);
+    for (int k = 0; k < 200; ++k) {
+      sess.step(default_stepsize(5, 4), 1);
+      SolverState st = sess.state(false);
+      CHECK(std::abs(st.r.sum() - st.s.sum()) <= 1e-10);
+    }
+  });
+  run("warm restart from a converged state is stationary", [] {  // :251-270
+    Rng rng(13);
+    Problem pr = random_problem(rng, 3, 3);
+    QuadraticReg reg(0.5);
+    SolverOptions opt;
+    opt.tol_primal = 1e-10;
+    opt.max_iter = 500000;
+    SolveReport rep = solve(pr, reg, opt);
+    CHECK(rep.termination == Termination::Converged);
+    SolverState st = make_state(pr, WarmStart{rep.state.X, rep.state.phi, rep.state.psi});
+    Matrix before = st.X;
+    step(st, pr, reg, rep.rho);
+    CHECK(max_abs_diff(st.X, before) <= 1e-8);
+    CHECK(std::max(norm(st.r), norm(st.s)) <= 1e-8);
+  });
+  run("stall detection fires after a fixed no-improvement window", [] {  // :272-286
+    Rng rng(17);
+    Problem pr = random_problem(rng, 3, 3);
+    GroupLassoReg pin(1e9, column_class_blocks({0, 0, 0}, 3));  // iterate pinned at zero
+    SolverOptions opt;
+    opt.max_iter = 30000;
+    SolveReport rep = solve(pr, pin, opt);
+    CHECK(rep.termination == Termination::Stalled);
+    CHECK(rep.iterations == 10001);
+    CHECK(rep.r_primal > 0.1);
+  });
+  run("overflowing iterates are reported", [] {  // :288-301
+    Matrix c(1, 2);
+    c << 0.1, 0.9;
+    Problem pr = validate_problem(c, Vector::Ones(1), Vector::Constant(2, 0.5));
+    SolverOptions opt;
+    opt.init = WarmStart{Matrix::Constant(1, 2, 1e308), Vector::Zero(1), Vector::Zero(2)};
+    CHECK(throws_as<NonFiniteIterate>([&] { solve(pr, ZeroReg(), opt); }));
+  });
+  run("warm-start validation", [] {  // :326-339
+    Matrix c(2, 2);
+    c << 0.0, 1.0, 1.0, 0.0;
+    Problem pr = validate_problem(c, Vector{0.5, 0.5}, Vector{0.5, 0.5});
+    SolverOptions opt;
+    opt.init = WarmStart{Matrix::Zero(3, 2), Vector::Zero(3), Vector::Zero(2)};
+    CHECK(throws_as<DimensionMismatch>([&] { solve(pr, ZeroReg(), opt); }));
+    opt.init = WarmStart{Matrix::Constant(2, 2, -0.1), Vector::Zero(2), Vector::Zero(2)};
+    CHECK(throws_as<NegativeEntry>([&] { solve(pr, ZeroReg(), opt); }));
+  });
+  run("fused kernel reproduces the reference path", [] {  // :342-357
+    Rng rng(19);
+    for (int trial = 0; trial < 5; ++trial) {
+      Problem pr = random_problem(rng, 4, 5);
+      QuadraticReg reg(0.4);
+      SolverOptions opt;
+      opt.max_iter = 501;
+      opt.tol_primal = 1e-300;
+      SolveReport a = solve(pr, reg, opt);
+      opt.fused = true;
+      SolveReport b = solve(pr, reg, opt);
+      CHECK(a.iterations == b.iterations);
+      CHECK(max_abs_diff(a.plan(), b.plan()) <= 1e-12);
+    }
+  });
+  run("solves are equivariant under row and column permutations", [] {  // :359-391
+    Rng rng(23);
+    Problem pr = random_problem(rng, 4, 5);
+    const Index sigma[4] = {2, 0, 3, 1};
+    const Index tau[5] = {4, 2, 0, 1, 3};
+    Matrix cp(4, 5);
+    Vector pp(4), qp(5);
+    for (Index i = 0; i < 4; ++i) {
+      pp[i] = pr.p[sigma[i]];
+      for (Index j = 0; j < 5; ++j) cp(i, j) = pr.cost(sigma[i], tau[j]);
+    }
+    for (Index j = 0; j < 5; ++j) qp[j] = pr.q[tau[j]];
+    Problem prp = validate_problem(cp, pp, qp);
+    SolverOptions opt;
+    opt.tol_primal = 1e-9;
+    opt.max_iter = 400000;
+    SolveReport rep = solve(pr, QuadraticReg(1.0), opt);
+    SolveReport repp = solve(prp, QuadraticReg(1.0), opt);
+    double worst = 0.0;
+    for (Index i = 0; i < 4; ++i)
+      for (Index j = 0; j < 5; ++j)
+        worst = std::max(worst, std::abs(repp.plan()(i, j) - rep.plan()(sigma[i], tau[j])));
+    CHECK(worst <= 1e-6);
+  });
+  run("moderate problems converge under sparse and smooth penalties", [] {  // :393-412
+    Rng rng(29);
+    const Index n = 20;
+    Problem pr = random_problem(rng, n, n);
+    std::vector<int> labels(static_cast<std::size_t>(n));
+    for (Index i = 0; i < n; ++i) labels[static_cast<std::size_t>(i)] = static_cast<int>(i % 4);
+    std::vector<std::unique_ptr<Regularizer>> regs;
+    regs.emplace_back(new ZeroReg());
+    regs.emplace_back(new QuadraticReg(0.05));
+    regs.emplace_back(new GroupLassoReg(0.01, column_class_blocks(labels, n)));
+    for (auto& reg : regs) {
+      SolverOptions opt;
+      opt.tol_primal = 1e-6;
+      opt.max_iter = 200000;
+      SolveReport rep = solve(pr, *reg, opt);
+      CHECK(rep.termination == Termination::Converged);
+      CHECK(rep.r_primal < 1e-6);
+    }
+  });
+  run("trace records settled support and certificate columns", [] {  // :414-440
+    Rng rng(41);
+    Problem pr = random_problem(rng, 20, 20);
+    SolverOptions opt;
+    opt.tol_primal = 1e-7;
+    opt.max_iter = 200000;
+    opt.record_trace = true;
+    opt.check_every = 10;
+    SolveReport rep = solve(pr, QuadraticReg(0.05), opt);
+    CHECK(rep.termination == Termination::Converged);
+    CHECK(!rep.trace.empty());
+    CHECK(rep.support_last_change >= 0 && rep.support_last_change < rep.iterations);
+    const long final_support = rep.trace.back().support;
+    for (const TraceRow& row : rep.trace) {
+      CHECK(row.iter % 10 == 0);
+      CHECK(std::isfinite(row.gap) && std::isfinite(row.dual_residual));
+      if (row.iter > rep.support_last_change) CHECK(row.support == final_support);
+    }
+    CHECK(rep.trace.back().r_primal <= 1e-7);
+  });
+  run("certificate wiring: hand-computed 1x1 state", [] {  // test_duality.cpp:68-86
+    Matrix c(1, 1);
+    c << 0.2;
+    Problem pr = validate_problem(c, Vector::Ones(1), Vector::Ones(1));
+    SolverState st = make_state(pr, WarmStart{Matrix::Ones(1, 1), Vector::Constant(1, 0.5),
+                                              Vector::Constant(1, 0.25)});
+    DualCertificate cert = duality_gap(pr, ZeroReg(), st, 0.5);
+    CHECK(std::abs(cert.mu[0] - 1.0) <= 1e-15 && std::abs(cert.nu[0] - 0.5) <= 1e-15);
+    CHECK(std::abs(cert.dual_value - 1.5) <= 1e-14);
+    CHECK(std::abs(cert.gap - (0.2 - 1.5)) <= 1e-14);
+    CHECK(std::abs(cert.dual_residual - 0.65) <= 1e-14);
+  });
+  run("primal objective formulas", [] {  // test_problem.cpp:160-176
+    Matrix c(2, 2), x(2, 2);
+    c << 0, 1, 1, 0;
+    x << 0.5, 0, 0, 0.5;
+    Problem pr = validate_problem(c, Vector{0.5, 0.5}, Vector{0.5, 0.5});
+    CHECK(primal_objective(pr, x, ZeroReg()) == 0.0);
+    Matrix c1(1, 1), x1(1, 1);
+    c1 << 1.0;
+    x1 << 1.0;
+    Problem one = validate_problem(c1, Vector::Ones(1), Vector::Ones(1));
+    CHECK(std::abs(primal_objective(one, x1, QuadraticReg(2.0)) - 2.0) <= 1e-15);
+    CHECK(throws_as<DimensionMismatch>([&] { primal_objective(pr, Matrix::Zero(2, 3), ZeroReg()); }));
+  });
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  const bool cpu_only = argc > 1 && std::strcmp(argv[1], "--cpu") == 0;
+  host_cases();
+  if (cpu_only) {
+    if (!otdr_dev_cuda_available()) no_gpu_case();
+  } else {
+    device_cases();
+  }
+  std::printf("%d checks, %d failures\n", checks, failures);
+  return failures;
+}
