@@ -129,9 +129,9 @@ class ClockSampler:
 
 
 def shard_rows(rank, world):
-    lo = M * rank // world
-    hi = M * (rank + 1) // world
-    return lo, hi
+    from paper_2305_18483_b200 import sharding
+
+    return sharding.row_bands(M, world)[rank]
 
 
 def init_dist(world, local_rank):
@@ -156,20 +156,9 @@ def max_over_ranks(dist, value: float) -> float:
 
 
 def bcast_nccl_id(dist, rank):
-    from paper_2305_18483_b200 import _native as nat
+    from paper_2305_18483_b200 import sharding
 
-    buf = bytearray(128)
-    if rank == 0:
-        import ctypes as ct
-
-        raw = ct.create_string_buffer(128)
-        rc = nat.lib().otdr_dev_nccl_unique_id(raw)
-        if rc:
-            raise RuntimeError("ncclGetUniqueId failed")
-        buf = bytearray(raw.raw)
-    obj = [bytes(buf)]
-    dist.broadcast_object_list(obj, src=0)
-    return obj[0]
+    return sharding.broadcast_nccl_id(dist, rank)
 
 
 def make_engine(rank, world, dist, local_rank):
