@@ -131,20 +131,59 @@ struct otdr_dev {
   // geometry
   int stripes = 1, rowgroups = 1, rows_per_cta = 1;
   int gl_stripes = 1, num_segs = 0, cert_stripes = 1, num_cert_segs = 0;
+  // single-pass cluster GL sweep plan (0 = use the two-phase fallback kernel)
+  int glc_tn = 0, glc_k = 1, glc_rows = 0;
+  size_t glc_smem = 0;
   int RB = 1, CB = 1;
   size_t rowpart_cap = 0, colpart_cap = 0, cpart_cap = 0;
   std::vector<Segment> segs, cert_segs;
 
-  // graphs keyed by (kind, unroll/chunk, track, cert)
-  std::map<std::tuple<int, int, int, int>, cudaGraphExec_t> graphs;
+  // graphs keyed by (kind, unroll/chunk, track, cert, fused)
+  std::map<std::tuple<int, int, int, int, int>, cudaGraphExec_t> graphs;
 
   bool f64() const { return storage == OTDR_STORE_F64; }
   int tn_seg() const { return f64() ? 64 : 128; }  // GL / certificate stripe width
 
   // ---------------------------------------------------------------- launches
+  template <typename T, bool EXACT, int VW>
+  void launch_gl_cluster() {
+    auto kern = otdrk::gl_cluster_kernel<T, EXACT, VW>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(glc_smem)));
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(unsigned(gl_stripes * glc_k), unsigned(num_segs), 1);
+    lc.blockDim = dim3(otdrk::kThreads, 1, 1);
+    lc.dynamicSmemBytes = glc_smem;
+    lc.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(glc_k);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    otdrk::GLArgs<T> ga{(T*)X, (const T*)C, phi, psi, rowpart, colpart, d_seg, d_prm, d_ctl,
+                        m_loc, ld};
+    CK(cudaLaunchKernelEx(&lc, kern, ga, glc_k, glc_rows));
+  }
+
+  // The cluster kernel covers the plain (non-fused, untracked) iteration; the
+  // even/odd and support-tracking variants use the two-phase kernel.
+  bool gl_cluster_active(bool track) const { return glc_tn > 0 && !track && !prm.fused; }
+
   void launch_sweep(bool track, bool sums_only) {
+    if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only && gl_cluster_active(track)) {
+      if (f64()) {
+        if (glc_tn == 64) launch_gl_cluster<double, true, 2>();
+        else launch_gl_cluster<double, true, 1>();
+      } else {
+        if (glc_tn == 128) launch_gl_cluster<float, false, 4>();
+        else if (glc_tn == 64) launch_gl_cluster<float, false, 2>();
+        else launch_gl_cluster<float, false, 1>();
+      }
+      return;
+    }
     if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only) {
-      dim3 grid(gl_stripes, num_segs);
+      dim3 grid((unsigned)((ld + tn_seg() - 1) / tn_seg()), num_segs);
       if (f64()) {
         otdrk::GLArgs<double> ga{(double*)X, (const double*)C, phi, psi, rowpart, colpart,
                                  d_seg, d_prm, d_ctl, m_loc, ld};
@@ -185,10 +224,19 @@ struct otdr_dev {
 
   bool gl_active(bool sums_only) const { return reg_kind == OTDR_REG_GROUP_LASSO && !sums_only; }
 
-  void launch_reduce(bool sums_only) {
+  void launch_reduce(bool sums_only, bool track) {
+    int nstripes = stripes, ngroups = rowgroups;
+    if (gl_active(sums_only)) {
+      if (gl_cluster_active(track)) {
+        nstripes = gl_stripes;
+        ngroups = num_segs * glc_k;
+      } else {
+        nstripes = int((ld + tn_seg() - 1) / tn_seg());
+        ngroups = num_segs;
+      }
+    }
     otdrk::ReduceArgs ra{rowpart, colpart, p, r, exch, bpart, d_ctl, m_loc, n, ld,
-                         gl_active(sums_only) ? gl_stripes : stripes,
-                         gl_active(sums_only) ? num_segs : rowgroups, RB};
+                         nstripes, ngroups, RB};
     otdrk::reduce_kernel<<<RB + CB, otdrk::kThreads, 0, stream>>>(ra);
   }
 
@@ -225,7 +273,7 @@ struct otdr_dev {
   // One DR iteration: sweep, reduce, [all-reduce], update, [certificate].
   void launch_iteration(bool track, bool cert, cudaGraphConditionalHandle cond, int use_cond) {
     launch_sweep(track, false);
-    launch_reduce(false);
+    launch_reduce(false, track);
     launch_exchange(exch, size_t(n) + 3);
     launch_update(cond, use_cond, cert ? 1 : 0);
     if (cert) launch_cert(0, cond, use_cond);
@@ -242,7 +290,7 @@ struct otdr_dev {
     rows_per_cta = int((m_loc + rg - 1) / rg);
     rowgroups = int((m_loc + rows_per_cta - 1) / rows_per_cta);
     gl_stripes = int((ld + tn_seg() - 1) / tn_seg());
-    cert_stripes = gl_stripes;
+    cert_stripes = int((ld + tn_seg() - 1) / tn_seg());
     RB = int((m_loc + otdrk::kThreads - 1) / otdrk::kThreads);
     CB = int((n + otdrk::kThreads - 1) / otdrk::kThreads);
   }
@@ -280,6 +328,7 @@ struct otdr_dev {
     if (cert_segs.empty()) cert_segs.push_back(Segment{0, 0, 0, 0});
     num_segs = int(segs.size());
     num_cert_segs = int(cert_segs.size());
+    plan_gl_cluster();
     if (d_seg) cudaFree(d_seg);
     if (d_cert_seg) cudaFree(d_cert_seg);
     d_seg = dalloc<Segment>(segs.size());
@@ -290,9 +339,44 @@ struct otdr_dev {
     ensure_partials();
   }
 
+  // Largest stripe width whose segment tile fits a cluster of <= 8 CTAs with
+  // <= 96 KB of staged v per CTA (2 CTAs per SM).
+  void plan_gl_cluster() {
+    glc_tn = 0;
+    glc_k = 1;
+    glc_rows = 0;
+    glc_smem = 0;
+    gl_stripes = int((ld + tn_seg() - 1) / tn_seg());
+    if (reg_kind != OTDR_REG_GROUP_LASSO) return;
+    long long lmax = 0;
+    for (const Segment& sg : segs) lmax = std::max(lmax, sg.end - sg.begin);
+    if (lmax == 0) return;
+    const int cands_f32[3] = {128, 64, 32};
+    const int cands_f64[2] = {64, 32};
+    const int* cands = f64() ? cands_f64 : cands_f32;
+    const int nc = f64() ? 2 : 3;
+    for (int ci = 0; ci < nc && glc_tn == 0; ++ci) {
+      const int tn = cands[ci];
+      for (int k = 1; k <= 8; k *= 2) {
+        const long long rows = (lmax + k - 1) / k;
+        const size_t stage = size_t(rows) * size_t(tn) * esz;
+        if (stage <= size_t(96) * 1024) {
+          glc_tn = tn;
+          glc_k = k;
+          glc_rows = int(rows);
+          glc_smem = stage + size_t(otdrk::kWarps + 2) * size_t(tn) * sizeof(double);
+          gl_stripes = int((ld + tn - 1) / tn);
+          break;
+        }
+      }
+    }
+  }
+
   void ensure_partials() {
-    const size_t need_row = size_t(std::max(stripes, gl_stripes)) * size_t(std::max<long long>(m_loc, 1));
-    const size_t need_col = size_t(std::max(rowgroups, num_segs)) * size_t(ld);
+    const int seg_stripes = int((ld + tn_seg() - 1) / tn_seg());
+    const size_t need_row = size_t(std::max(std::max(stripes, gl_stripes), seg_stripes)) *
+                            size_t(std::max<long long>(m_loc, 1));
+    const size_t need_col = size_t(std::max(rowgroups, num_segs * std::max(glc_k, 1))) * size_t(ld);
     const size_t need_c = size_t(cert_stripes) * size_t(num_cert_segs) * otdrk::kCertVals;
     if (need_row > rowpart_cap) {
       if (rowpart) cudaFree(rowpart);
@@ -342,7 +426,7 @@ struct otdr_dev {
   // kind 0: plain chunk of `count` iterations; kind 1: WHILE loop whose body
   // is `count` iterations.
   cudaGraphExec_t get_graph(int kind, int count, bool track, bool cert) {
-    auto key = std::make_tuple(kind, count, track ? 1 : 0, cert ? 1 : 0);
+    auto key = std::make_tuple(kind, count, track ? 1 : 0, cert ? 1 : 0, prm.fused ? 1 : 0);
     auto it = graphs.find(key);
     if (it != graphs.end()) return it->second;
     cudaGraph_t g = nullptr;
@@ -460,7 +544,7 @@ struct otdr_dev {
     prm.fused = 0;
     push_prm();
     launch_sweep(false, true);
-    launch_reduce(true);
+    launch_reduce(true, false);
     launch_exchange(exch, size_t(n) + 3);
     otdrk::SeedArgs sa{exch, q, r, phi, psi, s, a, b, d_ctl, m_loc, m_glob, n};
     const long long cnt = std::max(m_loc, n);
@@ -850,7 +934,7 @@ otdr_status otdr_dev_profile(otdr_dev* ctx, double rho, int64_t iters, otdr_kern
       CK(cudaEventRecord(ev[0], ctx->stream));
       ctx->launch_sweep(false, false);
       CK(cudaEventRecord(ev[1], ctx->stream));
-      ctx->launch_reduce(false);
+      ctx->launch_reduce(false, false);
       CK(cudaEventRecord(ev[2], ctx->stream));
       ctx->launch_exchange(ctx->exch, size_t(ctx->n) + 3);
       CK(cudaEventRecord(ev[3], ctx->stream));

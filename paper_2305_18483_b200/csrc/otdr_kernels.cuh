@@ -16,6 +16,7 @@
 // bit-identical to the reference given identical inputs; only the order of the
 // row/column sums differs (fixed, deterministic, not Eigen's).
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -459,6 +460,161 @@ __global__ void __launch_bounds__(kThreads) gl_sweep_kernel(GLArgs<T> a) {
     if (lane == 0) {
       if (ws) atomicAdd(&a.ctl->supp_count, ws);
       if (wc) atomicOr(&a.ctl->supp_changed, 1);
+    }
+  }
+}
+
+// ------------------------------------- group-lasso sweep, single pass (cluster)
+// The B200 form of the group-lasso sweep: one thread-block CLUSTER of K CTAs
+// owns a (class segment, column stripe) tile; CTA k of the cluster owns rows
+// [begin + k*R, begin + (k+1)*R) of the segment. Phase 1 reads C and X once,
+// keeps the pre-prox values v in shared memory and reduces per-column partial
+// ||v_g||^2. The K partials are combined through distributed shared memory
+// (every CTA sums them in the same rank order, so all agree bit-for-bit), the
+// block soft-threshold scale is formed, and phase 2 scales the staged v and
+// writes X once: 12 B per entry in HBM (fp32 storage), no re-read.
+// Staging precision: T (fp64 storage stages fp64 -> element-wise identical to
+// the reference; fp32 storage stages fp32 v, <= 1 ulp(fp32) from v*sigma).
+template <typename T, bool EXACT, int VW>
+__global__ void __launch_bounds__(kThreads) gl_cluster_kernel(GLArgs<T> a, int K, int R) {
+  namespace cg = cooperative_groups;
+  constexpr int TN = 32 * VW;
+  const Ctl* ctl = a.ctl;
+  if (ctl->done) return;  // grid-uniform: every CTA of every cluster returns together
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* stage = reinterpret_cast<T*>(smem_raw);                    // R x TN
+  double* red = reinterpret_cast<double*>(stage + (size_t)R * TN);  // kWarps x TN
+  double* psq = red + kWarps * TN;                               // TN (read by the cluster)
+  double* sig = psq + TN;                                        // TN
+
+  const Params& prm = *a.prm;
+  const double rho = prm.rho, thr = prm.gl_thr;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long stripe = blockIdx.x / K;
+  const long long col0 = stripe * TN + lane * VW;
+  const bool cok = col0 < a.ld;
+  const Segment sg = a.seg[blockIdx.y];
+  const long long r0 = sg.begin + (long long)crank * R;
+  long long r1 = r0 + R;
+  if (r1 > sg.end) r1 = sg.end;
+
+  double psi_r[VW], sq[VW], cacc[VW];
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    psi_r[e] = cok ? a.psi[col0 + e] : 0.0;
+    sq[e] = 0.0;
+    cacc[e] = 0.0;
+  }
+
+  // phase 1: v = [((X - rho C) + phi) + psi]_+ -> smem, per-column sum of v^2.
+  // U rows per warp in flight (loads issued before any use).
+  constexpr int U = 4;
+  for (long long i0 = r0 + warp; i0 < r1; i0 += (long long)kWarps * U) {
+    if (!cok) break;
+    double x[U][VW], c[U][VW], ph[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + (long long)u * kWarps;
+      if (i < r1) {
+        ph[u] = a.phi[i];
+        if constexpr (VW == 4) {
+          unpack(ld_rw(reinterpret_cast<const float4*>(a.X + i * a.ld + col0)), x[u]);
+          unpack(ld_ro(reinterpret_cast<const float4*>(a.C + i * a.ld + col0)), c[u]);
+        } else if constexpr (VW == 2 && sizeof(T) == 8) {
+          unpack(ld_rw(reinterpret_cast<const double2*>(a.X + i * a.ld + col0)), x[u]);
+          unpack(ld_ro(reinterpret_cast<const double2*>(a.C + i * a.ld + col0)), c[u]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < VW; ++e) {
+            x[u][e] = (double)a.X[i * a.ld + col0 + e];
+            c[u][e] = (double)__ldg(a.C + i * a.ld + col0 + e);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + (long long)u * kWarps;
+      if (i >= r1) break;
+      T* srow = stage + (size_t)(i - r0) * TN + lane * VW;
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[u][e], __dmul_rn(rho, c[u][e])), ph[u]), psi_r[e])
+                                 : (fma(-rho, c[u][e], x[u][e]) + ph[u]) + psi_r[e];
+        const double v = clamp0(val);
+        srow[e] = (T)v;
+        sq[e] += v * v;
+      }
+    }
+  }
+  if (sg.grouped) {
+#pragma unroll
+    for (int e = 0; e < VW; ++e) red[warp * TN + lane * VW + e] = sq[e];
+  }
+  __syncthreads();
+  if (sg.grouped) {
+    for (int t = threadIdx.x; t < TN; t += kThreads) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) s += red[w * TN + t];
+      psq[t] = s;
+    }
+  }
+  cluster.sync();  // partial norms of every CTA visible cluster-wide
+  if (sg.grouped) {
+    for (int t = threadIdx.x; t < TN; t += kThreads) {
+      double s = 0.0;
+      for (int k = 0; k < K; ++k) s += *cluster.map_shared_rank(psq + t, k);  // fixed rank order
+      const double nrm = sqrt(s);
+      sig[t] = (nrm <= thr) ? 0.0 : (EXACT ? __dsub_rn(1.0, __ddiv_rn(thr, nrm)) : 1.0 - thr / nrm);
+    }
+  } else {
+    for (int t = threadIdx.x; t < TN; t += kThreads) sig[t] = 1.0;
+  }
+  cluster.sync();  // remote reads done (psq may be retired) and sigma visible
+  double sc[VW];
+#pragma unroll
+  for (int e = 0; e < VW; ++e) sc[e] = sig[lane * VW + e];
+
+  // phase 2: X = v * sigma, row partials, column partials
+  for (long long i = r0 + warp; i < r1; i += kWarps) {
+    double rs = 0.0;
+    if (cok) {
+      const T* srow = stage + (size_t)(i - r0) * TN + lane * VW;
+      double o[VW];
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        const double v = (double)srow[e];
+        const double nx = sg.grouped ? (EXACT ? __dmul_rn(v, sc[e]) : v * sc[e]) : v;
+        o[e] = nx;
+        cacc[e] += nx;
+        rs += nx;
+      }
+      if constexpr (VW == 4) {
+        *reinterpret_cast<float4*>(a.X + i * a.ld + col0) = pack4(o);
+      } else if constexpr (VW == 2 && sizeof(T) == 8) {
+        *reinterpret_cast<double2*>(a.X + i * a.ld + col0) = pack2(o);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VW; ++e) a.X[i * a.ld + col0 + e] = (T)o[e];
+      }
+    }
+    rs = warp_sum(rs);
+    if (lane == 0) a.rowpart[stripe * a.m + i] = rs;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < VW; ++e) red[warp * TN + lane * VW + e] = cacc[e];
+  __syncthreads();
+  for (int t = threadIdx.x; t < TN; t += kThreads) {
+    const long long col = stripe * TN + t;
+    if (col < a.ld) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) s += red[w * TN + t];
+      a.colpart[((long long)blockIdx.y * K + crank) * a.ld + col] = s;
     }
   }
 }

@@ -369,3 +369,46 @@ def test_large_fp32_properties(ora):
     assert (g.X >= 0).all()
     assert abs(g.r.sum() - g.s.sum()) <= 1e-9
     np.testing.assert_allclose(g.X.sum(axis=1) - p, g.r, atol=1e-9)
+
+
+@pytest.mark.parametrize("storage,m,n,classes", [
+    ("f64", 3000, 300, 2),    # cluster of 8 CTAs per class segment (DSMEM norms)
+    ("f32", 3000, 301, 2),
+    ("f32", 1000, 1000, 10),  # the cfg3 shape at 1/10 scale
+    ("f64", 4000, 64, 1),     # segment too long for a cluster: two-phase fallback
+])
+def test_gl_long_segments_match_oracle(ora, storage, m, n, classes):
+    C, p, q, src, tgt, ls, lt = ora.adaptation_problem(m, n, classes, 3)
+    Co = C if storage == "f64" else C.astype(np.float32).astype(np.float64)
+    pr = ora.Problem(Co, p, q)
+    offs, cells = ora.column_class_blocks(ls, n)
+    oreg = ora.group_lasso_reg(1e-3, offs, cells)
+    st = ora.make_state(pr)
+    eng = otdr.Engine(m, n, storage)
+    eng.set_problem(C, p, q)
+    eng.set_regularizer(otdr.GroupLassoReg(1e-3, otdr.column_class_blocks(ls, n)))
+    eng.set_state()
+    rho = ora.default_stepsize(m, n)
+    for _ in range(12):
+        ora.step(st, pr, oreg, rho)
+    eng.step(rho, 12)
+    g = eng.get_state()
+    tol = 1e-12 if storage == "f64" else 1e-5
+    assert rel(g.X, st.X) <= tol, rel(g.X, st.X)
+    assert rel(g.phi, st.phi) <= tol and rel(g.psi, st.psi) <= tol
+
+
+def test_gl_fused_and_trace_match_unfused(ora):
+    C, p, q, src, tgt, ls, lt = ora.adaptation_problem(200, 150, 3, 5)
+    pr = otdr.Problem(C, p, q)
+    reg = otdr.GroupLassoReg(2e-3, otdr.column_class_blocks(ls, 150))
+    a = otdr.solve(pr, reg, otdr.SolverOptions(max_iter=301, tol_primal=1e-300))
+    b = otdr.solve(pr, reg, otdr.SolverOptions(max_iter=301, tol_primal=1e-300, fused=True))
+    c = otdr.solve(pr, reg, otdr.SolverOptions(max_iter=301, tol_primal=1e-300, record_trace=True,
+                                               check_every=50, deterministic=True))
+    assert a.iterations == b.iterations == c.iterations == 301
+    assert rel(b.plan(), a.plan()) <= 1e-12 and rel(c.plan(), a.plan()) <= 1e-12
+    o = ora.solve(ora.Problem(C, p, q), ora.group_lasso_reg(2e-3, *ora.column_class_blocks(ls, 150)),
+                  max_iter=301, tol_primal=1e-300, record_trace=True, check_every=50, deterministic=True)
+    assert [r.support for r in c.trace] == [r[4] for r in o.trace]
+    assert c.support_last_change == o.support_last_change
