@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -354,10 +355,19 @@ struct otdr_dev {
     const int cands_f32[3] = {128, 64, 32};
     const int cands_f64[2] = {64, 32};
     const int* cands = f64() ? cands_f64 : cands_f32;
-    const int nc = f64() ? 2 : 3;
+    int nc = f64() ? 2 : 3;
+    int kmin = 1;
+    // Tuning hook: OTDR_GL_PLAN="tn,kmin" pins the stripe width / minimum
+    // cluster size; OTDR_GL_PLAN="off" forces the two-phase kernel.
+    int env_tn = 0;
+    if (const char* e = std::getenv("OTDR_GL_PLAN")) {
+      if (std::strcmp(e, "off") == 0) return;
+      std::sscanf(e, "%d,%d", &env_tn, &kmin);
+    }
     for (int ci = 0; ci < nc && glc_tn == 0; ++ci) {
       const int tn = cands[ci];
-      for (int k = 1; k <= 8; k *= 2) {
+      if (env_tn && tn != env_tn) continue;
+      for (int k = std::max(1, kmin); k <= 8; k *= 2) {
         const long long rows = (lmax + k - 1) / k;
         const size_t stage = size_t(rows) * size_t(tn) * esz;
         if (stage <= size_t(96) * 1024) {
