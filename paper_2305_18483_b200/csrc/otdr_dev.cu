@@ -9,6 +9,8 @@
 #include "otdr_dev.h"
 #include "otdr_kernels.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -110,7 +112,8 @@ struct otdr_dev {
   double *p = nullptr, *q = nullptr, *phi = nullptr, *psi = nullptr, *a = nullptr, *b = nullptr,
          *r = nullptr, *s = nullptr;
   double *rowpart = nullptr, *colpart = nullptr, *exch = nullptr, *bpart = nullptr,
-         *cpart = nullptr, *csum = nullptr, *stage = nullptr;
+         *cpart = nullptr, *csum = nullptr, *stage = nullptr, *fpart = nullptr, *fpart2 = nullptr;
+  int num_sms = 148, fin_grid = 1;
   long long* d_dev_row = nullptr;
   Segment *d_seg = nullptr, *d_cert_seg = nullptr;
   Params* d_prm = nullptr;
@@ -135,6 +138,7 @@ struct otdr_dev {
   // single-pass cluster GL sweep plan (0 = use the two-phase fallback kernel)
   int glc_tn = 0, glc_k = 1, glc_rows = 0;
   size_t glc_smem = 0;
+  CUtensorMap glc_mapX{}, glc_mapC{};
   int RB = 1, CB = 1;
   size_t rowpart_cap = 0, colpart_cap = 0, cpart_cap = 0;
   std::vector<Segment> segs, cert_segs;
@@ -146,10 +150,11 @@ struct otdr_dev {
   int tn_seg() const { return f64() ? 64 : 128; }  // GL / certificate stripe width
 
   // ---------------------------------------------------------------- launches
-  template <typename T, bool EXACT, int VW>
+  template <typename T, bool EXACT>
   void launch_gl_cluster() {
-    auto kern = otdrk::gl_cluster_kernel<T, EXACT, VW>;
+    auto kern = otdrk::gl_cluster_kernel<T, EXACT>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(glc_smem)));
+    if (glc_k > 8) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(unsigned(gl_stripes * glc_k), unsigned(num_segs), 1);
     lc.blockDim = dim3(otdrk::kThreads, 1, 1);
@@ -164,7 +169,30 @@ struct otdr_dev {
     lc.numAttrs = 1;
     otdrk::GLArgs<T> ga{(T*)X, (const T*)C, phi, psi, rowpart, colpart, d_seg, d_prm, d_ctl,
                         m_loc, ld};
-    CK(cudaLaunchKernelEx(&lc, kern, ga, glc_k, glc_rows));
+    CK(cudaLaunchKernelEx(&lc, kern, ga, glc_mapX, glc_mapC, glc_k, glc_rows));
+  }
+
+  // 2-D tensor map over a row-major (m_loc x ld) matrix, box TN x R.
+  void encode_map(CUtensorMap* map, void* base, int tn, int rows) {
+    static PFN_cuTensorMapEncodeTiled encode = [] {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+              cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        fn = nullptr;
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+    }();
+    if (!encode) throw Error{OTDR_E_CUDA, "cuTensorMapEncodeTiled unavailable"};
+    const cuuint64_t dims[2] = {cuuint64_t(ld), cuuint64_t(std::max<long long>(m_loc, 1))};
+    const cuuint64_t strides[1] = {cuuint64_t(ld) * esz};
+    const cuuint32_t box[2] = {cuuint32_t(tn), cuuint32_t(rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(map, f64() ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                              2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error{OTDR_E_CUDA, "cuTensorMapEncodeTiled failed"};
   }
 
   // The cluster kernel covers the plain (non-fused, untracked) iteration; the
@@ -173,14 +201,8 @@ struct otdr_dev {
 
   void launch_sweep(bool track, bool sums_only) {
     if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only && gl_cluster_active(track)) {
-      if (f64()) {
-        if (glc_tn == 64) launch_gl_cluster<double, true, 2>();
-        else launch_gl_cluster<double, true, 1>();
-      } else {
-        if (glc_tn == 128) launch_gl_cluster<float, false, 4>();
-        else if (glc_tn == 64) launch_gl_cluster<float, false, 2>();
-        else launch_gl_cluster<float, false, 1>();
-      }
+      if (f64()) launch_gl_cluster<double, true>();
+      else launch_gl_cluster<float, false>();
       return;
     }
     if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only) {
@@ -225,17 +247,18 @@ struct otdr_dev {
 
   bool gl_active(bool sums_only) const { return reg_kind == OTDR_REG_GROUP_LASSO && !sums_only; }
 
-  void launch_reduce(bool sums_only, bool track) {
-    int nstripes = stripes, ngroups = rowgroups;
+  // (stripes of the row partials, row groups of the column partials) written
+  // by the sweep variant that runs in this configuration.
+  std::pair<int, int> partial_shape(bool sums_only, bool track) const {
     if (gl_active(sums_only)) {
-      if (gl_cluster_active(track)) {
-        nstripes = gl_stripes;
-        ngroups = num_segs * glc_k;
-      } else {
-        nstripes = int((ld + tn_seg() - 1) / tn_seg());
-        ngroups = num_segs;
-      }
+      if (gl_cluster_active(track)) return {gl_stripes, num_segs * glc_k};
+      return {int((ld + tn_seg() - 1) / tn_seg()), num_segs};
     }
+    return {stripes, rowgroups};
+  }
+
+  void launch_reduce(bool sums_only, bool track) {
+    const auto [nstripes, ngroups] = partial_shape(sums_only, track);
     otdrk::ReduceArgs ra{rowpart, colpart, p, r, exch, bpart, d_ctl, m_loc, n, ld,
                          nstripes, ngroups, RB};
     otdrk::reduce_kernel<<<RB + CB, otdrk::kThreads, 0, stream>>>(ra);
@@ -271,12 +294,36 @@ struct otdr_dev {
     otdrk::cert_final_kernel<<<1, otdrk::kThreads, 0, stream>>>(fa);
   }
 
-  // One DR iteration: sweep, reduce, [all-reduce], update, [certificate].
+  // Single GPU: reduce + update fused into one cooperative launch.
+  void launch_finalize(bool track, cudaGraphConditionalHandle cond, int use_cond, int cert_follows) {
+    const auto [nstripes, ngroups] = partial_shape(false, track);
+    otdrk::FinalizeArgs fa{rowpart, colpart, p, q, r, s, phi, psi, a, b, exch, fpart, fpart2,
+                           d_prm, d_ctl, m_loc, n, ld, nstripes, ngroups, cond, use_cond,
+                           cert_follows};
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(unsigned(fin_grid), 1, 1);
+    lc.blockDim = dim3(otdrk::kThreads, 1, 1);
+    lc.dynamicSmemBytes = 0;
+    lc.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, otdrk::finalize_kernel, fa));
+  }
+
+  // One DR iteration: sweep, then (single GPU) the fused finalize, or (row
+  // shards) reduce, all-reduce of the exchange vector, update; [certificate].
   void launch_iteration(bool track, bool cert, cudaGraphConditionalHandle cond, int use_cond) {
     launch_sweep(track, false);
-    launch_reduce(false, track);
-    launch_exchange(exch, size_t(n) + 3);
-    launch_update(cond, use_cond, cert ? 1 : 0);
+    if (comm == nullptr) {
+      launch_finalize(track, cond, use_cond, cert ? 1 : 0);
+    } else {
+      launch_reduce(false, track);
+      launch_exchange(exch, size_t(n) + 3);
+      launch_update(cond, use_cond, cert ? 1 : 0);
+    }
     if (cert) launch_cert(0, cond, use_cond);
   }
 
@@ -340,46 +387,38 @@ struct otdr_dev {
     ensure_partials();
   }
 
-  // Largest stripe width whose segment tile fits a cluster of <= 8 CTAs with
-  // <= 96 KB of staged v per CTA (2 CTAs per SM).
+  // TMA tile plan: 256-byte column stripes (64 fp32 / 32 fp64), R <= 256 rows
+  // per CTA (TMA box limit), clusters of K <= 8 CTAs (16 non-portable) per
+  // class segment; prefer <= ~70 KB of shared memory (3 CTAs per SM).
   void plan_gl_cluster() {
     glc_tn = 0;
     glc_k = 1;
     glc_rows = 0;
     glc_smem = 0;
     gl_stripes = int((ld + tn_seg() - 1) / tn_seg());
-    if (reg_kind != OTDR_REG_GROUP_LASSO) return;
+    if (reg_kind != OTDR_REG_GROUP_LASSO || m_loc == 0) return;
     long long lmax = 0;
     for (const Segment& sg : segs) lmax = std::max(lmax, sg.end - sg.begin);
     if (lmax == 0) return;
-    const int cands_f32[3] = {128, 64, 32};
-    const int cands_f64[2] = {64, 32};
-    const int* cands = f64() ? cands_f64 : cands_f32;
-    int nc = f64() ? 2 : 3;
-    int kmin = 1;
-    // Tuning hook: OTDR_GL_PLAN="tn,kmin" pins the stripe width / minimum
-    // cluster size; OTDR_GL_PLAN="off" forces the two-phase kernel.
-    int env_tn = 0;
-    if (const char* e = std::getenv("OTDR_GL_PLAN")) {
-      if (std::strcmp(e, "off") == 0) return;
-      std::sscanf(e, "%d,%d", &env_tn, &kmin);
+    int rows_soft = 140;
+    int kmin = 1, kmax = 16;
+    // Tuning hook: OTDR_GL_PLAN="rows_soft,kmin" or "off" (two-phase kernel).
+    if (const char* ev = std::getenv("OTDR_GL_PLAN")) {
+      if (std::strcmp(ev, "off") == 0) return;
+      std::sscanf(ev, "%d,%d", &rows_soft, &kmin);
     }
-    for (int ci = 0; ci < nc && glc_tn == 0; ++ci) {
-      const int tn = cands[ci];
-      if (env_tn && tn != env_tn) continue;
-      for (int k = std::max(1, kmin); k <= 8; k *= 2) {
-        const long long rows = (lmax + k - 1) / k;
-        const size_t stage = size_t(rows) * size_t(tn) * esz;
-        if (stage <= size_t(96) * 1024) {
-          glc_tn = tn;
-          glc_k = k;
-          glc_rows = int(rows);
-          glc_smem = stage + size_t(otdrk::kWarps + 2) * size_t(tn) * sizeof(double);
-          gl_stripes = int((ld + tn - 1) / tn);
-          break;
-        }
-      }
-    }
+    const int tn = int(256 / esz);
+    int k = std::max(1, kmin);
+    while (k < kmax && (lmax + k - 1) / k > rows_soft) k *= 2;
+    const long long rows = (lmax + k - 1) / k;
+    if (rows > 256) return;  // segment too long: two-phase kernel
+    glc_tn = tn;
+    glc_k = k;
+    glc_rows = int(rows);
+    glc_smem = 2 * size_t(rows) * 256 + size_t(otdrk::kWarps + 2) * size_t(tn) * 8 + 16;
+    gl_stripes = int((ld + tn - 1) / tn);
+    encode_map(&glc_mapX, X, tn, glc_rows);
+    encode_map(&glc_mapC, C, tn, glc_rows);
   }
 
   void ensure_partials() {
@@ -567,7 +606,7 @@ struct otdr_dev {
   void release() {
     invalidate_graphs();
     void* ptrs[] = {C, X, p, q, phi, psi, a, b, r, s, rowpart, colpart, exch, bpart, cpart,
-                    csum, stage, d_dev_row, d_seg, d_cert_seg, d_prm, d_ctl, d_trace, d_mx};
+                    csum, stage, fpart, fpart2, d_dev_row, d_seg, d_cert_seg, d_prm, d_ctl, d_trace, d_mx};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);
     if (h_ctl) cudaFreeHost(h_ctl);
@@ -620,8 +659,7 @@ int otdr_dev_cuda_available(void) {
 const char* otdr_dev_last_error(const otdr_dev* ctx) { return ctx ? ctx->err.c_str() : ""; }
 
 int otdr_dev_kernels_per_iteration(const otdr_dev* ctx) {
-  (void)ctx;
-  return 3;
+  return (ctx && ctx->comm) ? 3 : 2;  // sweep + finalize (single GPU) / + reduce, update
 }
 
 otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
@@ -669,6 +707,18 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     CK(cudaMemset(ctx->b, 0, size_t(ctx->ld) * 8));
     CK(cudaMemset(ctx->s, 0, size_t(ctx->ld) * 8));
     ctx->exch = dalloc<double>(size_t(ctx->n) + 3);
+    CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
+    {
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, otdrk::finalize_kernel,
+                                                       otdrk::kThreads, 0));
+      const long long want = std::max<long long>(
+          1, (std::max(ctx->m_loc, ctx->n) + otdrk::kThreads - 1) / otdrk::kThreads);
+      ctx->fin_grid = int(std::min<long long>(want, (long long)ctx->num_sms * std::max(occ, 1)));
+      ctx->fin_grid = std::min(ctx->fin_grid, ctx->num_sms);
+      ctx->fpart = dalloc<double>(size_t(ctx->fin_grid) * 3);
+      ctx->fpart2 = dalloc<double>(size_t(ctx->fin_grid));
+    }
     ctx->plan_geometry();
     ctx->bpart = dalloc<double>(size_t(ctx->RB + ctx->CB) * 3);
     ctx->csum = dalloc<double>(otdrk::kCertVals);
@@ -944,11 +994,17 @@ otdr_status otdr_dev_profile(otdr_dev* ctx, double rho, int64_t iters, otdr_kern
       CK(cudaEventRecord(ev[0], ctx->stream));
       ctx->launch_sweep(false, false);
       CK(cudaEventRecord(ev[1], ctx->stream));
-      ctx->launch_reduce(false, false);
-      CK(cudaEventRecord(ev[2], ctx->stream));
-      ctx->launch_exchange(ctx->exch, size_t(ctx->n) + 3);
-      CK(cudaEventRecord(ev[3], ctx->stream));
-      ctx->launch_update(0, 0, 0);
+      if (ctx->comm == nullptr) {  // reduce_ms reports the fused finalize kernel
+        ctx->launch_finalize(false, 0, 0, 0);
+        CK(cudaEventRecord(ev[2], ctx->stream));
+        CK(cudaEventRecord(ev[3], ctx->stream));
+      } else {
+        ctx->launch_reduce(false, false);
+        CK(cudaEventRecord(ev[2], ctx->stream));
+        ctx->launch_exchange(ctx->exch, size_t(ctx->n) + 3);
+        CK(cudaEventRecord(ev[3], ctx->stream));
+        ctx->launch_update(0, 0, 0);
+      }
       CK(cudaEventRecord(ev[4], ctx->stream));
       ctx->check_launch();
       CK(cudaEventSynchronize(ev[4]));

@@ -17,6 +17,7 @@
 // row/column sums differs (fixed, deterministic, not Eigen's).
 #pragma once
 #include <cooperative_groups.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -70,8 +71,10 @@ struct Ctl {
   long long support_last_change;
   long long trace_len;
   unsigned long long t0_ns;
-  double objective, gap, dres, dual_value;
+  double objective, gap, dual_value, dres;
   long long last_support;
+  unsigned int bar_count;  // grid barrier of the cooperative finalize kernel
+  unsigned int bar_gen;
 };
 
 struct TraceRow {
@@ -133,7 +136,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // CTA (blockIdx.x = stripe, blockIdx.y = row group) owns columns
 // [stripe*TN, stripe*TN+TN) of rows [rg*rows_per_cta, ...). Lane l holds NV
 // vectors at columns stripe*TN + v*32*VEC + l*VEC (coalesced 512 B per warp
-// per vector slot). Row partials: warp butterfly -> rowpart[stripe][row].
+// per vector slot). Row partials: warp butterfly -> rowpart[row][stripe].
 // Column partials: registers over the CTA's rows, then a fixed-order
 // cross-warp smem sum -> colpart[rg][col].
 template <typename T>
@@ -142,7 +145,7 @@ struct SweepArgs {
   const T* C;
   const double* phi;
   const double* psi;
-  double* rowpart;  // [stripes][m]
+  double* rowpart;  // [m][stripes]
   double* colpart;  // [rowgroups][ld]
   const Params* prm;
   Ctl* ctl;
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(SweepArgs<T> a) {
           reinterpret_cast<V*>(a.X + i * a.ld)[cols[v] / VEC] = pack<T>(o);
       }
       rs = warp_sum(rs);
-      if (lane == 0) a.rowpart[stripe * a.m + i] = rs;
+      if (lane == 0) a.rowpart[i * (long long)gridDim.x + stripe] = rs;
     }
   }
 
@@ -306,7 +309,7 @@ struct GLArgs {
   const T* C;
   const double* phi;
   const double* psi;
-  double* rowpart;  // [stripes][m]
+  double* rowpart;  // [m][stripes]
   double* colpart;  // [segments][ld]
   const Segment* seg;
   const Params* prm;
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(kThreads) gl_sweep_kernel(GLArgs<T> a) {
       xrow[cols[v] / VEC] = pack<T>(o);
     }
     rs = warp_sum(rs);
-    if (lane == 0) a.rowpart[stripe * a.m + i] = rs;
+    if (lane == 0) a.rowpart[i * (long long)gridDim.x + stripe] = rs;
   }
   __syncthreads();
 #pragma unroll
@@ -465,41 +468,95 @@ __global__ void __launch_bounds__(kThreads) gl_sweep_kernel(GLArgs<T> a) {
 }
 
 // ------------------------------------- group-lasso sweep, single pass (cluster)
-// The B200 form of the group-lasso sweep: one thread-block CLUSTER of K CTAs
-// owns a (class segment, column stripe) tile; CTA k of the cluster owns rows
-// [begin + k*R, begin + (k+1)*R) of the segment. Phase 1 reads C and X once,
-// keeps the pre-prox values v in shared memory and reduces per-column partial
-// ||v_g||^2. The K partials are combined through distributed shared memory
-// (every CTA sums them in the same rank order, so all agree bit-for-bit), the
-// block soft-threshold scale is formed, and phase 2 scales the staged v and
-// writes X once: 12 B per entry in HBM (fp32 storage), no re-read.
-// Staging precision: T (fp64 storage stages fp64 -> element-wise identical to
-// the reference; fp32 storage stages fp32 v, <= 1 ulp(fp32) from v*sigma).
-template <typename T, bool EXACT, int VW>
-__global__ void __launch_bounds__(kThreads) gl_cluster_kernel(GLArgs<T> a, int K, int R) {
+// The B200 form of the group-lasso sweep. One thread-block CLUSTER of K CTAs
+// owns a (class segment, 256-byte column stripe) tile; CTA k of the cluster
+// owns R rows of the segment. Its C and X tiles (R x TN) arrive in shared
+// memory through two 2-D TMA loads (cp.async.bulk.tensor, mbarrier
+// completion), so all of the CTA's bytes are in flight at once with no
+// register staging. Phase 1 computes v = [((X - rho C) + phi) + psi]_+ from the
+// tiles, overwrites the X tile with v and reduces per-column ||v_g||^2. The K
+// partial norms are combined through distributed shared memory (every CTA sums
+// them in the same rank order, so all agree bit-for-bit), the block
+// soft-threshold scale is formed (regularizers.cpp:85-99), and phase 2 writes
+// X = v * scale once: 12 B per entry of HBM traffic in fp32 storage.
+// Staging precision is T: fp64 storage stages fp64 v (element-wise identical
+// to the reference); fp32 storage stages fp32 v (<= 1 ulp(fp32) from v*scale).
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+      : "memory");
+}
+
+template <typename T, bool EXACT>
+__global__ void __launch_bounds__(kThreads) gl_cluster_kernel(GLArgs<T> a,
+                                                             const __grid_constant__ CUtensorMap mapX,
+                                                             const __grid_constant__ CUtensorMap mapC,
+                                                             int K, int R) {
   namespace cg = cooperative_groups;
-  constexpr int TN = 32 * VW;
+  constexpr int TN = 256 / (int)sizeof(T);  // 64 floats / 32 doubles: one 256-byte box row
+  constexpr int VW = TN / 32;
   const Ctl* ctl = a.ctl;
   if (ctl->done) return;  // grid-uniform: every CTA of every cluster returns together
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = (int)cluster.block_rank();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* stage = reinterpret_cast<T*>(smem_raw);                    // R x TN
-  double* red = reinterpret_cast<double*>(stage + (size_t)R * TN);  // kWarps x TN
-  double* psq = red + kWarps * TN;                               // TN (read by the cluster)
-  double* sig = psq + TN;                                        // TN
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* tileX = reinterpret_cast<T*>(smem_raw);                 // R x TN (then v)
+  T* tileC = tileX + (size_t)R * TN;                          // R x TN
+  double* red = reinterpret_cast<double*>(tileC + (size_t)R * TN);  // kWarps x TN
+  double* psq = red + kWarps * TN;                            // TN (read by the cluster)
+  double* sig = psq + TN;                                     // TN
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sig + TN);
 
   const Params& prm = *a.prm;
   const double rho = prm.rho, thr = prm.gl_thr;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nstripes = gridDim.x / K;
   const long long stripe = blockIdx.x / K;
-  const long long col0 = stripe * TN + lane * VW;
+  const long long colbase = stripe * TN;
+  const long long col0 = colbase + lane * VW;
   const bool cok = col0 < a.ld;
   const Segment sg = a.seg[blockIdx.y];
   const long long r0 = sg.begin + (long long)crank * R;
   long long r1 = r0 + R;
   if (r1 > sg.end) r1 = sg.end;
+  const int nrows = r1 > r0 ? (int)(r1 - r0) : 0;
 
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    if (nrows > 0) {
+      // full boxes (rows past the segment / matrix and columns past ld are
+      // loaded or zero-filled, never used)
+      mbar_expect_tx(bar, 2u * (unsigned)(R * TN * sizeof(T)));
+      tma_load_2d(tileX, &mapX, (int)colbase, (int)r0, bar);
+      tma_load_2d(tileC, &mapC, (int)colbase, (int)r0, bar);
+    }
+  }
   double psi_r[VW], sq[VW], cacc[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
@@ -507,44 +564,27 @@ __global__ void __launch_bounds__(kThreads) gl_cluster_kernel(GLArgs<T> a, int K
     sq[e] = 0.0;
     cacc[e] = 0.0;
   }
+  __syncthreads();  // barrier initialised before anyone waits on it
+  if (nrows > 0) mbar_wait(bar, 0);
 
-  // phase 1: v = [((X - rho C) + phi) + psi]_+ -> smem, per-column sum of v^2.
-  // U rows per warp in flight (loads issued before any use).
-  constexpr int U = 4;
-  for (long long i0 = r0 + warp; i0 < r1; i0 += (long long)kWarps * U) {
-    if (!cok) break;
-    double x[U][VW], c[U][VW], ph[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = i0 + (long long)u * kWarps;
-      if (i < r1) {
-        ph[u] = a.phi[i];
-        if constexpr (VW == 4) {
-          unpack(ld_rw(reinterpret_cast<const float4*>(a.X + i * a.ld + col0)), x[u]);
-          unpack(ld_ro(reinterpret_cast<const float4*>(a.C + i * a.ld + col0)), c[u]);
-        } else if constexpr (VW == 2 && sizeof(T) == 8) {
-          unpack(ld_rw(reinterpret_cast<const double2*>(a.X + i * a.ld + col0)), x[u]);
-          unpack(ld_ro(reinterpret_cast<const double2*>(a.C + i * a.ld + col0)), c[u]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < VW; ++e) {
-            x[u][e] = (double)a.X[i * a.ld + col0 + e];
-            c[u][e] = (double)__ldg(a.C + i * a.ld + col0 + e);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = i0 + (long long)u * kWarps;
-      if (i >= r1) break;
-      T* srow = stage + (size_t)(i - r0) * TN + lane * VW;
+  // phase 1 (from shared memory)
+  if (cok) {
+    for (int t = warp; t < nrows; t += kWarps) {
+      const double ph = a.phi[r0 + t];
+      T* xr = tileX + (size_t)t * TN + lane * VW;
+      const T* cr = tileC + (size_t)t * TN + lane * VW;
+      double x[VW], c[VW];
 #pragma unroll
       for (int e = 0; e < VW; ++e) {
-        const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[u][e], __dmul_rn(rho, c[u][e])), ph[u]), psi_r[e])
-                                 : (fma(-rho, c[u][e], x[u][e]) + ph[u]) + psi_r[e];
+        x[e] = (double)xr[e];
+        c[e] = (double)cr[e];
+      }
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, c[e])), ph), psi_r[e])
+                                 : (fma(-rho, c[e], x[e]) + ph) + psi_r[e];
         const double v = clamp0(val);
-        srow[e] = (T)v;
+        xr[e] = (T)v;
         sq[e] += v * v;
       }
     }
@@ -573,43 +613,43 @@ __global__ void __launch_bounds__(kThreads) gl_cluster_kernel(GLArgs<T> a, int K
   } else {
     for (int t = threadIdx.x; t < TN; t += kThreads) sig[t] = 1.0;
   }
-  cluster.sync();  // remote reads done (psq may be retired) and sigma visible
+  cluster.sync();  // remote reads done (psq may be retired) and the scale visible
   double sc[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) sc[e] = sig[lane * VW + e];
 
-  // phase 2: X = v * sigma, row partials, column partials
-  for (long long i = r0 + warp; i < r1; i += kWarps) {
+  // phase 2: X = v * scale, row partials, column partials
+  for (int t = warp; t < nrows; t += kWarps) {
+    const long long i = r0 + t;
     double rs = 0.0;
     if (cok) {
-      const T* srow = stage + (size_t)(i - r0) * TN + lane * VW;
+      const T* vr = tileX + (size_t)t * TN + lane * VW;
       double o[VW];
 #pragma unroll
       for (int e = 0; e < VW; ++e) {
-        const double v = (double)srow[e];
+        const double v = (double)vr[e];
         const double nx = sg.grouped ? (EXACT ? __dmul_rn(v, sc[e]) : v * sc[e]) : v;
         o[e] = nx;
         cacc[e] += nx;
         rs += nx;
       }
-      if constexpr (VW == 4) {
-        *reinterpret_cast<float4*>(a.X + i * a.ld + col0) = pack4(o);
-      } else if constexpr (VW == 2 && sizeof(T) == 8) {
-        *reinterpret_cast<double2*>(a.X + i * a.ld + col0) = pack2(o);
+      if constexpr (VW == 2 && sizeof(T) == 4) {
+        *reinterpret_cast<float2*>(a.X + i * a.ld + col0) =
+            make_float2(__double2float_rn(o[0]), __double2float_rn(o[1]));
       } else {
 #pragma unroll
         for (int e = 0; e < VW; ++e) a.X[i * a.ld + col0 + e] = (T)o[e];
       }
     }
     rs = warp_sum(rs);
-    if (lane == 0) a.rowpart[stripe * a.m + i] = rs;
+    if (lane == 0) a.rowpart[i * (long long)nstripes + stripe] = rs;
   }
   __syncthreads();
 #pragma unroll
   for (int e = 0; e < VW; ++e) red[warp * TN + lane * VW + e] = cacc[e];
   __syncthreads();
   for (int t = threadIdx.x; t < TN; t += kThreads) {
-    const long long col = stripe * TN + t;
+    const long long col = colbase + t;
     if (col < a.ld) {
       double s = 0.0;
 #pragma unroll
@@ -644,7 +684,7 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(ReduceArgs a) {
     const long long i = (long long)blockIdx.x * kThreads + threadIdx.x;
     double R = 0.0, r = 0.0;
     if (i < a.m) {
-      for (int s = 0; s < a.stripes; ++s) R += a.rowpart[(long long)s * a.m + i];
+      for (int s = 0; s < a.stripes; ++s) R += a.rowpart[i * a.stripes + s];
       r = R - a.p[i];
       a.r[i] = r;
     }
@@ -725,6 +765,46 @@ __device__ __forceinline__ void finish_iteration(Ctl* ctl, const Params& prm, lo
   }
 }
 
+// Bookkeeping after X_{k+1} and the residual norms: theta/eta/k, trace
+// support counters, and the solve loop's stopping logic (solver.cpp:179-235).
+__device__ void finish_solve_iteration(Ctl* ctl, const Params& prm, long long k, double theta,
+                                       double eta, double rp, int cert_follows,
+                                       cudaGraphConditionalHandle cond, int use_cond) {
+  ctl->theta[(k + 1) & 1] = __dsub_rn(theta, eta);
+  ctl->eta = eta;
+  ctl->k = k + 1;
+  ctl->r_primal = rp;
+  if (prm.fused) ctl->fused_shifted ^= 1;
+  const long long kk = k + 1 - ctl->k0;
+  if (prm.record_trace) {
+    if (ctl->supp_changed) ctl->support_last_change = kk;
+    ctl->last_support = (long long)ctl->supp_count;
+    ctl->supp_changed = 0;
+    ctl->supp_count = 0;
+  }
+  if (prm.solving) {
+    if (!(rp - rp == 0.0)) {  // !isfinite  solver.cpp:181-185
+      ctl->done = 1;
+      ctl->termination = TERM_NONFINITE;
+    } else {
+      if (rp < ctl->best * (1.0 - 1e-14)) {  // solver.cpp:200-203
+        ctl->best = rp;
+        ctl->last_improvement = kk;
+      }
+      const bool at_check = (kk % prm.check_every) == 0;
+      const bool want_cert = (at_check && prm.has_tol_gap && rp <= prm.tol_primal) ||
+                             (prm.record_trace && (at_check || kk == prm.max_iter));
+      if (want_cert && cert_follows) {
+        ctl->want_cert = 1;  // the certificate kernels finish this iteration
+      } else {
+        const bool converged = at_check && rp <= prm.tol_primal && !prm.has_tol_gap;
+        finish_iteration(ctl, prm, kk, converged);
+      }
+    }
+    if (use_cond) cudaGraphSetConditional(cond, ctl->done ? 0u : 1u);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a) {
   Ctl* ctl = a.ctl;
   if (ctl->done) return;
@@ -772,39 +852,150 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a) {
   const double nr = sqrt(rsq), ns = sqrt(tssq);
   const double rp = (nr < ns) ? ns : nr;
   ctl->cnt_update = 0;
-  ctl->theta[(k + 1) & 1] = __dsub_rn(theta, eta);
-  ctl->eta = eta;
-  ctl->k = k + 1;
-  ctl->r_primal = rp;
-  if (prm.fused) ctl->fused_shifted ^= 1;
-  const long long kk = k + 1 - ctl->k0;
-  if (prm.record_trace) {
-    if (ctl->supp_changed) ctl->support_last_change = kk;
-    ctl->last_support = (long long)ctl->supp_count;
-    ctl->supp_changed = 0;
-    ctl->supp_count = 0;
-  }
-  if (prm.solving) {
-    if (!(rp - rp == 0.0)) {  // !isfinite  solver.cpp:181-185
-      ctl->done = 1;
-      ctl->termination = TERM_NONFINITE;
+  finish_solve_iteration(ctl, prm, k, theta, eta, rp, a.cert_follows, a.cond, a.use_cond);
+}
+
+// ------------------------------------------------------------- finalize
+// Single-GPU fusion of reduce + update: one cooperative launch (every CTA
+// co-resident) with one software grid barrier between the sums and the
+// recurrence. Row sums are read warp-per-row from the [row][stripe] partials
+// (coalesced), column sums thread-per-column from [group][col]. Every CTA folds
+// the per-CTA partials in the same order, so eta/shift agree bit-for-bit; the
+// last CTA to finish applies the stopping logic (solver.cpp:179-235).
+struct FinalizeArgs {
+  const double* rowpart;  // [m][stripes]
+  const double* colpart;  // [groups][ld]
+  const double* p;
+  const double* q;
+  double* r;
+  double* s;
+  double* phi;
+  double* psi;
+  double* a;
+  double* b;
+  double* S;              // column sums scratch [n]
+  double* part;           // [gridDim.x * 3]
+  double* part2;          // [gridDim.x]
+  const Params* prm;
+  Ctl* ctl;
+  long long m, n, ld;
+  int stripes, groups;
+  cudaGraphConditionalHandle cond;
+  int use_cond;
+  int cert_follows;
+};
+
+__device__ __forceinline__ void grid_barrier(Ctl* ctl) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = &ctl->bar_gen;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1) {
+      ctl->bar_count = 0;
+      __threadfence();
+      atomicAdd(&ctl->bar_gen, 1u);
     } else {
-      if (rp < ctl->best * (1.0 - 1e-14)) {  // solver.cpp:200-203
-        ctl->best = rp;
-        ctl->last_improvement = kk;
-      }
-      const bool at_check = (kk % prm.check_every) == 0;
-      const bool want_cert = (at_check && prm.has_tol_gap && rp <= prm.tol_primal) ||
-                             (prm.record_trace && (at_check || kk == prm.max_iter));
-      if (want_cert && a.cert_follows) {
-        ctl->want_cert = 1;  // the certificate kernels finish this iteration
-      } else {
-        const bool converged = at_check && rp <= prm.tol_primal && !prm.has_tol_gap;
-        finish_iteration(ctl, prm, kk, converged);
+      while (*gen == g) {
       }
     }
-    if (a.use_cond) cudaGraphSetConditional(a.cond, ctl->done ? 0u : 1u);
+    __threadfence();
   }
+  __syncthreads();
+}
+
+__device__ void finish_solve_iteration(Ctl* ctl, const Params& prm, long long k, double theta,
+                                       double eta, double rp, int cert_follows,
+                                       cudaGraphConditionalHandle cond, int use_cond);
+
+__global__ void __launch_bounds__(kThreads) finalize_kernel(FinalizeArgs a) {
+  Ctl* ctl = a.ctl;
+  if (ctl->done) return;  // grid-uniform
+  const Params& prm = *a.prm;
+  __shared__ double red[kWarps];
+  __shared__ double sc[3];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long gwarp = (long long)blockIdx.x * kWarps + warp;
+  const long long nwarps = (long long)gridDim.x * kWarps;
+  // phase 1: rows (warp per row)
+  double sr = 0.0, sr2 = 0.0, sR = 0.0;
+  for (long long i = gwarp; i < a.m; i += nwarps) {
+    double R = 0.0;
+    for (int t = lane; t < a.stripes; t += 32) R += a.rowpart[i * a.stripes + t];
+    R = warp_sum(R);
+    const double ri = R - a.p[i];
+    if (lane == 0) a.r[i] = ri;
+    sr += ri;
+    sr2 += ri * ri;
+    sR += R;
+  }
+  // columns (thread per column, same mapping reused in phase 2)
+  const long long tid = (long long)blockIdx.x * kThreads + threadIdx.x;
+  const long long nthr = (long long)gridDim.x * kThreads;
+  for (long long j = tid; j < a.n; j += nthr) {
+    double S = 0.0;
+    for (int g = 0; g < a.groups; ++g) S += a.colpart[(long long)g * a.ld + j];
+    a.S[j] = S;
+  }
+  // lane 0 of each warp holds that warp's row sums (all lanes hold the same)
+  const double t1 = block_sum(lane == 0 ? sr : 0.0, red);
+  const double t2 = block_sum(lane == 0 ? sr2 : 0.0, red);
+  const double t3 = block_sum(lane == 0 ? sR : 0.0, red);
+  if (threadIdx.x == 0) {
+    a.part[blockIdx.x * 3 + 0] = t1;
+    a.part[blockIdx.x * 3 + 1] = t2;
+    a.part[blockIdx.x * 3 + 2] = t3;
+  }
+  grid_barrier(ctl);
+  if (threadIdx.x == 0) {
+    double u1 = 0.0, u2 = 0.0, u3 = 0.0;
+    for (unsigned c = 0; c < gridDim.x; ++c) {
+      u1 += __ldcg(a.part + c * 3 + 0);
+      u2 += __ldcg(a.part + c * 3 + 1);
+      u3 += __ldcg(a.part + c * 3 + 2);
+    }
+    sc[0] = u1;
+    sc[1] = u2;
+    sc[2] = u3;
+  }
+  __syncthreads();
+  const long long k = ctl->k;
+  const double theta = ctl->theta[k & 1];
+  const double mn = (double)(a.m + a.n);
+  const double eta = __ddiv_rn(sc[0], mn);
+  const double shift = __dsub_rn(2.0 * eta, theta);
+  const double dn = (double)a.n, dm = (double)a.m;
+  // phase 2: recurrence (solver.cpp:28-37)
+  for (long long i = tid; i < a.m; i += nthr) {
+    const double ri = __ldcg(a.r + i), ai = a.a[i];
+    a.phi[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift), dn);
+    a.a[i] = __dsub_rn(ai, ri);
+  }
+  double ssq = 0.0;
+  for (long long j = tid; j < a.n; j += nthr) {
+    const double sj = __dsub_rn(a.S[j], a.q[j]);
+    const double bj = a.b[j];
+    a.s[j] = sj;
+    a.psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift), dm);
+    a.b[j] = __dsub_rn(bj, sj);
+    ssq += sj * sj;
+  }
+  const double bs = block_sum(ssq, red);
+  if (threadIdx.x == 0) {
+    a.part2[blockIdx.x] = bs;
+    __threadfence();
+    last = atomicAdd(&ctl->cnt_update, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double tssq = 0.0;
+  for (unsigned c = 0; c < gridDim.x; ++c) tssq += __ldcg(a.part2 + c);
+  ctl->cnt_update = 0;
+  const double nr = sqrt(sc[1]), ns = sqrt(tssq);
+  const double rp = (nr < ns) ? ns : nr;  // std::max semantics (solver.cpp:179)
+  finish_solve_iteration(ctl, prm, k, theta, eta, rp, a.cert_follows, a.cond, a.use_cond);
 }
 
 // ------------------------------------------------------ certificate / objective
