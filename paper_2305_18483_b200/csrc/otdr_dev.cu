@@ -8,6 +8,7 @@
 // Multi-rank contexts (NCCL inside the body) use host-polled chunk graphs.
 #include "otdr_dev.h"
 #include "otdr_kernels.cuh"
+#include "otdr_resident.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -114,6 +115,14 @@ struct otdr_dev {
   double *rowpart = nullptr, *colpart = nullptr, *exch = nullptr, *bpart = nullptr,
          *cpart = nullptr, *csum = nullptr, *stage = nullptr, *fpart = nullptr, *fpart2 = nullptr;
   int num_sms = 148, fin_grid = 1;
+  // single GPU: one cooperative finalize launch instead of reduce + update
+  // (OTDR_FINALIZE=fused opts in; measured slower than reduce + update on B200)
+  bool use_fused_finalize = false;
+  // on-chip resident solve (plans that fit the GPU's aggregate shared memory)
+  bool allow_resident = true;
+  int res_G = 0, res_R = 0;
+  size_t res_smem = 0;
+  double* gscratch = nullptr;
   long long* d_dev_row = nullptr;
   Segment *d_seg = nullptr, *d_cert_seg = nullptr;
   Params* d_prm = nullptr;
@@ -150,14 +159,16 @@ struct otdr_dev {
   int tn_seg() const { return f64() ? 64 : 128; }  // GL / certificate stripe width
 
   // ---------------------------------------------------------------- launches
-  template <typename T, bool EXACT>
+  static constexpr int kGLThreads = 512;
+
+  template <typename T, bool EXACT, int VW>
   void launch_gl_cluster() {
-    auto kern = otdrk::gl_cluster_kernel<T, EXACT>;
+    auto kern = otdrk::gl_cluster_kernel<T, EXACT, VW, kGLThreads>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(glc_smem)));
     if (glc_k > 8) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(unsigned(gl_stripes * glc_k), unsigned(num_segs), 1);
-    lc.blockDim = dim3(otdrk::kThreads, 1, 1);
+    lc.blockDim = dim3(kGLThreads, 1, 1);
     lc.dynamicSmemBytes = glc_smem;
     lc.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -201,8 +212,13 @@ struct otdr_dev {
 
   void launch_sweep(bool track, bool sums_only) {
     if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only && gl_cluster_active(track)) {
-      if (f64()) launch_gl_cluster<double, true>();
-      else launch_gl_cluster<float, false>();
+      if (f64()) {
+        if (glc_tn == 64) launch_gl_cluster<double, true, 2>();
+        else launch_gl_cluster<double, true, 1>();
+      } else {
+        if (glc_tn == 128) launch_gl_cluster<float, false, 4>();
+        else launch_gl_cluster<float, false, 2>();
+      }
       return;
     }
     if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only) {
@@ -317,7 +333,7 @@ struct otdr_dev {
   // shards) reduce, all-reduce of the exchange vector, update; [certificate].
   void launch_iteration(bool track, bool cert, cudaGraphConditionalHandle cond, int use_cond) {
     launch_sweep(track, false);
-    if (comm == nullptr) {
+    if (comm == nullptr && use_fused_finalize) {
       launch_finalize(track, cond, use_cond, cert ? 1 : 0);
     } else {
       launch_reduce(false, track);
@@ -377,6 +393,7 @@ struct otdr_dev {
     num_segs = int(segs.size());
     num_cert_segs = int(cert_segs.size());
     plan_gl_cluster();
+    plan_resident();
     if (d_seg) cudaFree(d_seg);
     if (d_cert_seg) cudaFree(d_cert_seg);
     d_seg = dalloc<Segment>(segs.size());
@@ -387,9 +404,58 @@ struct otdr_dev {
     ensure_partials();
   }
 
-  // TMA tile plan: 256-byte column stripes (64 fp32 / 32 fp64), R <= 256 rows
-  // per CTA (TMA box limit), clusters of K <= 8 CTAs (16 non-portable) per
-  // class segment; prefer <= ~70 KB of shared memory (3 CTAs per SM).
+  // Resident plan: one CTA per SM owning R = ceil(m / G) rows of C and X in
+  // shared memory for the whole solve (single rank, zero/quadratic).
+  void plan_resident() {
+    res_G = 0;
+    res_R = 0;
+    res_smem = 0;
+    if (!allow_resident || comm || m_loc < 1 || reg_kind == OTDR_REG_GROUP_LASSO) return;
+    int max_smem = 0;
+    CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg.device));
+    const long long G = std::min<long long>(num_sms, m_loc);
+    const long long R = (m_loc + G - 1) / G;
+    const size_t bytes = f64() ? otdrk::resident_smem_bytes<double>(R, n, ld)
+                               : otdrk::resident_smem_bytes<float>(R, n, ld);
+    if (bytes + 2048 > size_t(max_smem)) return;
+    res_G = int((m_loc + R - 1) / R);
+    res_R = int(R);
+    res_smem = bytes;
+    if (!gscratch) gscratch = dalloc<double>(size_t(num_sms) * size_t(n + 4));
+  }
+
+  bool resident_active(bool track, bool cert) const {
+    return res_G > 0 && !track && !cert && !prm.fused;
+  }
+
+  void launch_resident(long long iters) {
+    otdrk::ResidentArgs ra{X, C, 0, phi, a, r, p, psi, b, s, q, d_ctl, d_prm, gscratch,
+                           m_loc, n, ld, res_R, res_G,
+                           reg_kind == OTDR_REG_QUAD ? otdrk::REG_QUAD : otdrk::REG_NONE, iters};
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(unsigned(res_G), 1, 1);
+    lc.blockDim = dim3(otdrk::kThreads, 1, 1);
+    lc.dynamicSmemBytes = res_smem;
+    lc.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    if (f64()) {
+      auto kern = otdrk::resident_kernel<double, false>;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(res_smem)));
+      CK(cudaLaunchKernelEx(&lc, kern, ra));
+    } else {
+      auto kern = otdrk::resident_kernel<float, false>;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(res_smem)));
+      CK(cudaLaunchKernelEx(&lc, kern, ra));
+    }
+  }
+
+  // TMA tile plan: column stripes of 512 B (else 256 B) per box row, R <= 256
+  // rows per CTA (TMA box limit), a cluster of K <= 16 CTAs per class
+  // segment, <= ~72 KB of tiles per CTA so three CTAs share an SM.
   void plan_gl_cluster() {
     glc_tn = 0;
     glc_k = 1;
@@ -400,25 +466,37 @@ struct otdr_dev {
     long long lmax = 0;
     for (const Segment& sg : segs) lmax = std::max(lmax, sg.end - sg.begin);
     if (lmax == 0) return;
-    int rows_soft = 140;
-    int kmin = 1, kmax = 16;
-    // Tuning hook: OTDR_GL_PLAN="rows_soft,kmin" or "off" (two-phase kernel).
+    size_t tile_budget = 72 * 1024;
+    int kmin = 1;
+    int force_row_bytes = 0;
+    // Tuning hook: OTDR_GL_PLAN="tile_kb,kmin,row_bytes" or "off" (two-phase kernel).
     if (const char* ev = std::getenv("OTDR_GL_PLAN")) {
       if (std::strcmp(ev, "off") == 0) return;
-      std::sscanf(ev, "%d,%d", &rows_soft, &kmin);
+      int kb = 72;
+      std::sscanf(ev, "%d,%d,%d", &kb, &kmin, &force_row_bytes);
+      tile_budget = size_t(kb) * 1024;
     }
-    const int tn = int(256 / esz);
-    int k = std::max(1, kmin);
-    while (k < kmax && (lmax + k - 1) / k > rows_soft) k *= 2;
-    const long long rows = (lmax + k - 1) / k;
-    if (rows > 256) return;  // segment too long: two-phase kernel
-    glc_tn = tn;
-    glc_k = k;
-    glc_rows = int(rows);
-    glc_smem = 2 * size_t(rows) * 256 + size_t(otdrk::kWarps + 2) * size_t(tn) * 8 + 16;
-    gl_stripes = int((ld + tn - 1) / tn);
-    encode_map(&glc_mapX, X, tn, glc_rows);
-    encode_map(&glc_mapC, C, tn, glc_rows);
+    for (int row_bytes : {512, 256}) {
+      if (force_row_bytes && row_bytes != force_row_bytes) continue;
+      const int tn = int(row_bytes / esz);
+      const long long rows_max =
+          std::min<long long>(256, (long long)(tile_budget / (2 * size_t(row_bytes))));
+      int k = std::max(1, kmin);
+      while (k < 16 && (lmax + k - 1) / k > rows_max) k *= 2;
+      const long long rows = (lmax + k - 1) / k;
+      if (rows > rows_max) continue;
+      glc_tn = tn;
+      glc_k = k;
+      glc_rows = int(rows);
+      const size_t creg = std::max(size_t(rows) * size_t(row_bytes),
+                                   size_t(kGLThreads / 32) * size_t(tn) * 8);
+      glc_smem = size_t(rows) * size_t(row_bytes) + creg + 2 * size_t(tn) * 8 +
+                 size_t(rows) * 8 + 16;
+      gl_stripes = int((ld + tn - 1) / tn);
+      encode_map(&glc_mapX, X, tn, glc_rows);
+      encode_map(&glc_mapC, C, tn, glc_rows);
+      return;
+    }
   }
 
   void ensure_partials() {
@@ -509,6 +587,11 @@ struct otdr_dev {
 
   // Raw iterations (step): graph chunks plus a directly launched remainder.
   void run_raw(long long iters) {
+    if (iters > 0 && resident_active(false, false)) {
+      launch_resident(iters);
+      check_launch();
+      return;
+    }
     const int chunk = 16;
     if (iters >= chunk) {
       cudaGraphExec_t ex = get_graph(0, chunk, false, false);
@@ -606,7 +689,7 @@ struct otdr_dev {
   void release() {
     invalidate_graphs();
     void* ptrs[] = {C, X, p, q, phi, psi, a, b, r, s, rowpart, colpart, exch, bpart, cpart,
-                    csum, stage, fpart, fpart2, d_dev_row, d_seg, d_cert_seg, d_prm, d_ctl, d_trace, d_mx};
+                    csum, stage, fpart, fpart2, gscratch, d_dev_row, d_seg, d_cert_seg, d_prm, d_ctl, d_trace, d_mx};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);
     if (h_ctl) cudaFreeHost(h_ctl);
@@ -659,7 +742,8 @@ int otdr_dev_cuda_available(void) {
 const char* otdr_dev_last_error(const otdr_dev* ctx) { return ctx ? ctx->err.c_str() : ""; }
 
 int otdr_dev_kernels_per_iteration(const otdr_dev* ctx) {
-  return (ctx && ctx->comm) ? 3 : 2;  // sweep + finalize (single GPU) / + reduce, update
+  // sweep + finalize (single GPU) / sweep + reduce + update
+  return (ctx && (ctx->comm || !ctx->use_fused_finalize)) ? 3 : 2;
 }
 
 otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
@@ -708,14 +792,17 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     CK(cudaMemset(ctx->s, 0, size_t(ctx->ld) * 8));
     ctx->exch = dalloc<double>(size_t(ctx->n) + 3);
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
+    if (const char* fe = std::getenv("OTDR_FINALIZE")) ctx->use_fused_finalize = std::strcmp(fe, "fused") == 0;
+    if (const char* re = std::getenv("OTDR_RESIDENT")) ctx->allow_resident = std::strcmp(re, "off") != 0;
     {
       int occ = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, otdrk::finalize_kernel,
                                                        otdrk::kThreads, 0));
+      // enough warps for one warp per row in a single pass (rows read their
+      // stripe partials warp-wide), capped at full co-residency
       const long long want = std::max<long long>(
-          1, (std::max(ctx->m_loc, ctx->n) + otdrk::kThreads - 1) / otdrk::kThreads);
+          1, (std::max(ctx->m_loc, ctx->n) + otdrk::kWarps - 1) / otdrk::kWarps);
       ctx->fin_grid = int(std::min<long long>(want, (long long)ctx->num_sms * std::max(occ, 1)));
-      ctx->fin_grid = std::min(ctx->fin_grid, ctx->num_sms);
       ctx->fpart = dalloc<double>(size_t(ctx->fin_grid) * 3);
       ctx->fpart2 = dalloc<double>(size_t(ctx->fin_grid));
     }
@@ -994,7 +1081,7 @@ otdr_status otdr_dev_profile(otdr_dev* ctx, double rho, int64_t iters, otdr_kern
       CK(cudaEventRecord(ev[0], ctx->stream));
       ctx->launch_sweep(false, false);
       CK(cudaEventRecord(ev[1], ctx->stream));
-      if (ctx->comm == nullptr) {  // reduce_ms reports the fused finalize kernel
+      if (ctx->comm == nullptr && ctx->use_fused_finalize) {  // reduce_ms = fused finalize
         ctx->launch_finalize(false, 0, 0, 0);
         CK(cudaEventRecord(ev[2], ctx->stream));
         CK(cudaEventRecord(ev[3], ctx->stream));
@@ -1079,13 +1166,18 @@ otdr_status otdr_dev_solve(otdr_dev* ctx, const otdr_solve_opts* o, otdr_solve_r
     // The support mask of X_0 (solver.cpp:133-143) is implicit: the tracking
     // sweep compares each entry's old and new sign.
     CK(cudaStreamSynchronize(ctx->stream));
+    const bool resident = ctx->resident_active(track, cert);
     const bool use_while = ctx->comm == nullptr;
     const int body = 4;
-    cudaGraphExec_t ex = use_while ? ctx->get_graph(1, body, track, cert)
-                                   : ctx->get_graph(0, 8, track, cert);
+    cudaGraphExec_t ex = nullptr;
+    if (!resident)
+      ex = use_while ? ctx->get_graph(1, body, track, cert) : ctx->get_graph(0, 8, track, cert);
     CK(cudaEventRecord(ctx->ev0, ctx->stream));
     otdrk::stamp_t0_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_ctl);
-    if (use_while) {
+    if (resident) {
+      ctx->launch_resident(0);
+      ctx->check_launch();
+    } else if (use_while) {
       CK(cudaGraphLaunch(ex, ctx->stream));
     } else {
       for (;;) {

@@ -513,25 +513,27 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-template <typename T, bool EXACT>
-__global__ void __launch_bounds__(kThreads) gl_cluster_kernel(GLArgs<T> a,
-                                                             const __grid_constant__ CUtensorMap mapX,
-                                                             const __grid_constant__ CUtensorMap mapC,
-                                                             int K, int R) {
+template <typename T, bool EXACT, int VW, int NT>
+__global__ void __launch_bounds__(NT) gl_cluster_kernel(GLArgs<T> a,
+                                                       const __grid_constant__ CUtensorMap mapX,
+                                                       const __grid_constant__ CUtensorMap mapC,
+                                                       int K, int R) {
   namespace cg = cooperative_groups;
-  constexpr int TN = 256 / (int)sizeof(T);  // 64 floats / 32 doubles: one 256-byte box row
-  constexpr int VW = TN / 32;
+  constexpr int TN = 32 * VW;  // one TMA box row: 256 or 512 bytes
+  constexpr int NW = NT / 32;
   const Ctl* ctl = a.ctl;
   if (ctl->done) return;  // grid-uniform: every CTA of every cluster returns together
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = (int)cluster.block_rank();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* tileX = reinterpret_cast<T*>(smem_raw);                 // R x TN (then v)
-  T* tileC = tileX + (size_t)R * TN;                          // R x TN
-  double* red = reinterpret_cast<double*>(tileC + (size_t)R * TN);  // kWarps x TN
-  double* psq = red + kWarps * TN;                            // TN (read by the cluster)
+  T* tileC = tileX + (size_t)R * TN;                          // R x TN (then reduction scratch)
+  double* red = reinterpret_cast<double*>(tileC);             // NW x TN, after phase 1
+  const size_t creg = max((size_t)R * TN * sizeof(T), (size_t)NW * TN * sizeof(double));
+  double* psq = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(tileC) + creg);  // TN
   double* sig = psq + TN;                                     // TN
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sig + TN);
+  double* phs = sig + TN;                                     // R (phi of own rows)
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(phs + R);
 
   const Params& prm = *a.prm;
   const double rho = prm.rho, thr = prm.gl_thr;
@@ -557,6 +559,7 @@ __global__ void __launch_bounds__(kThreads) gl_cluster_kernel(GLArgs<T> a,
       tma_load_2d(tileC, &mapC, (int)colbase, (int)r0, bar);
     }
   }
+  for (int t = threadIdx.x; t < nrows; t += NT) phs[t] = a.phi[r0 + t];
   double psi_r[VW], sq[VW], cacc[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
@@ -564,54 +567,66 @@ __global__ void __launch_bounds__(kThreads) gl_cluster_kernel(GLArgs<T> a,
     sq[e] = 0.0;
     cacc[e] = 0.0;
   }
-  __syncthreads();  // barrier initialised before anyone waits on it
+  __syncthreads();  // barrier initialised and phi staged
   if (nrows > 0) mbar_wait(bar, 0);
 
-  // phase 1 (from shared memory)
+  // phase 1 (from shared memory): v -> X tile, per-column sum of v^2
   if (cok) {
-    for (int t = warp; t < nrows; t += kWarps) {
-      const double ph = a.phi[r0 + t];
+    for (int t = warp; t < nrows; t += NW) {
+      const double ph = phs[t];
       T* xr = tileX + (size_t)t * TN + lane * VW;
       const T* cr = tileC + (size_t)t * TN + lane * VW;
-      double x[VW], c[VW];
+      double x[VW], c[VW], o[VW];
+      if constexpr (VW * sizeof(T) == 16) {
+        unpack(*reinterpret_cast<const typename Vec<T>::type*>(xr), x);
+        unpack(*reinterpret_cast<const typename Vec<T>::type*>(cr), c);
+      } else {
 #pragma unroll
-      for (int e = 0; e < VW; ++e) {
-        x[e] = (double)xr[e];
-        c[e] = (double)cr[e];
+        for (int e = 0; e < VW; ++e) {
+          x[e] = (double)xr[e];
+          c[e] = (double)cr[e];
+        }
       }
 #pragma unroll
       for (int e = 0; e < VW; ++e) {
         const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, c[e])), ph), psi_r[e])
                                  : (fma(-rho, c[e], x[e]) + ph) + psi_r[e];
         const double v = clamp0(val);
-        xr[e] = (T)v;
+        o[e] = v;
         sq[e] += v * v;
+      }
+      if constexpr (VW * sizeof(T) == 16) {
+        *reinterpret_cast<typename Vec<T>::type*>(xr) = pack<T>(o);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VW; ++e) xr[e] = (T)o[e];
       }
     }
   }
+  __syncthreads();  // C tile no longer needed: reuse as reduction scratch
   if (sg.grouped) {
 #pragma unroll
     for (int e = 0; e < VW; ++e) red[warp * TN + lane * VW + e] = sq[e];
   }
   __syncthreads();
   if (sg.grouped) {
-    for (int t = threadIdx.x; t < TN; t += kThreads) {
+    for (int t = threadIdx.x; t < TN; t += NT) {
       double s = 0.0;
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) s += red[w * TN + t];
+      for (int w = 0; w < NW; ++w) s += red[w * TN + t];
       psq[t] = s;
     }
   }
   cluster.sync();  // partial norms of every CTA visible cluster-wide
   if (sg.grouped) {
-    for (int t = threadIdx.x; t < TN; t += kThreads) {
+    for (int t = threadIdx.x; t < TN; t += NT) {
       double s = 0.0;
       for (int k = 0; k < K; ++k) s += *cluster.map_shared_rank(psq + t, k);  // fixed rank order
       const double nrm = sqrt(s);
       sig[t] = (nrm <= thr) ? 0.0 : (EXACT ? __dsub_rn(1.0, __ddiv_rn(thr, nrm)) : 1.0 - thr / nrm);
     }
   } else {
-    for (int t = threadIdx.x; t < TN; t += kThreads) sig[t] = 1.0;
+    for (int t = threadIdx.x; t < TN; t += NT) sig[t] = 1.0;
   }
   cluster.sync();  // remote reads done (psq may be retired) and the scale visible
   double sc[VW];
@@ -619,21 +634,28 @@ __global__ void __launch_bounds__(kThreads) gl_cluster_kernel(GLArgs<T> a,
   for (int e = 0; e < VW; ++e) sc[e] = sig[lane * VW + e];
 
   // phase 2: X = v * scale, row partials, column partials
-  for (int t = warp; t < nrows; t += kWarps) {
+  for (int t = warp; t < nrows; t += NW) {
     const long long i = r0 + t;
     double rs = 0.0;
     if (cok) {
       const T* vr = tileX + (size_t)t * TN + lane * VW;
-      double o[VW];
+      double v[VW], o[VW];
+      if constexpr (VW * sizeof(T) == 16) {
+        unpack(*reinterpret_cast<const typename Vec<T>::type*>(vr), v);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VW; ++e) v[e] = (double)vr[e];
+      }
 #pragma unroll
       for (int e = 0; e < VW; ++e) {
-        const double v = (double)vr[e];
-        const double nx = sg.grouped ? (EXACT ? __dmul_rn(v, sc[e]) : v * sc[e]) : v;
+        const double nx = sg.grouped ? (EXACT ? __dmul_rn(v[e], sc[e]) : v[e] * sc[e]) : v[e];
         o[e] = nx;
         cacc[e] += nx;
         rs += nx;
       }
-      if constexpr (VW == 2 && sizeof(T) == 4) {
+      if constexpr (VW * sizeof(T) == 16) {
+        *reinterpret_cast<typename Vec<T>::type*>(a.X + i * a.ld + col0) = pack<T>(o);
+      } else if constexpr (VW == 2 && sizeof(T) == 4) {
         *reinterpret_cast<float2*>(a.X + i * a.ld + col0) =
             make_float2(__double2float_rn(o[0]), __double2float_rn(o[1]));
       } else {
@@ -648,12 +670,12 @@ __global__ void __launch_bounds__(kThreads) gl_cluster_kernel(GLArgs<T> a,
 #pragma unroll
   for (int e = 0; e < VW; ++e) red[warp * TN + lane * VW + e] = cacc[e];
   __syncthreads();
-  for (int t = threadIdx.x; t < TN; t += kThreads) {
+  for (int t = threadIdx.x; t < TN; t += NT) {
     const long long col = colbase + t;
     if (col < a.ld) {
       double s = 0.0;
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) s += red[w * TN + t];
+      for (int w = 0; w < NW; ++w) s += red[w * TN + t];
       a.colpart[((long long)blockIdx.y * K + crank) * a.ld + col] = s;
     }
   }

@@ -1,0 +1,342 @@
+// otdr_resident.cuh -- on-chip resident solve loop for plans that fit in the
+// aggregate shared memory of the GPU (grid mode) or of one thread-block
+// cluster (cluster mode, one problem per cluster: the batched entry point).
+//
+// Each CTA keeps its R rows of C and X in shared memory for the WHOLE solve:
+// HBM is touched once to load C/X and once to write the final plan back. One
+// DR iteration (solver.cpp:95-102, :23-38) per loop trip:
+//   1. sweep own rows in smem: clamp + prox, row sums (complete), per-CTA
+//      column sums; publish column sums + (sum r, sum r^2, sum X) partials
+//   2. exchange barrier
+//   3. column owner phase: CTA g owns a column slice, folds the G column
+//      partials in rank order, updates s, psi, b; every CTA folds the scalar
+//      partials (same order -> same eta/shift everywhere) and updates its phi/a
+//   4. exchange barrier; every CTA gathers psi and the sum s^2 partials, forms
+//      r_primal and runs the stopping logic (identical in every CTA)
+// Grid mode exchanges through global scratch (L2) with a software grid
+// barrier over co-resident CTAs (cooperative launch); cluster mode exchanges
+// through distributed shared memory with cluster barriers.
+#pragma once
+#include "otdr_kernels.cuh"
+
+namespace otdrk {
+
+struct ResidentArgs {
+  void* X;             // problem b at X + b * mat_stride (elements)
+  const void* C;
+  long long mat_stride;
+  double* phi;         // per-problem row vectors, stride m
+  double* a;
+  double* r;
+  const double* p;
+  double* psi;         // per-problem column vectors, stride n
+  double* b;
+  double* s;
+  const double* q;
+  Ctl* ctl;            // per problem
+  const Params* prm;
+  double* gscratch;    // grid mode: [G][n + 4] exchange rows
+  long long m, n, ld;
+  int R;               // rows per CTA
+  int G;               // CTAs per problem (grid size or cluster size)
+  int reg;             // REG_NONE / REG_QUAD
+  long long iters;     // raw mode: iterations to run (prm.solving == 0)
+};
+
+// Shared-memory layout (dynamic): C tile [R][ld] T | X tile [R][ld] T |
+// xrow: this CTA's exchange row [n + 4] doubles (column sums | sr | sr2 | sR | ssq)
+// | psi_s [n] | rowp [R][kWarps] | phi_s [R] | r_s [R]
+template <typename T>
+__host__ __device__ inline size_t resident_smem_bytes(long long R, long long n, long long ld) {
+  return size_t(2 * R * ld) * sizeof(T) + size_t(n + 4) * 8 + size_t(n) * 8 +
+         size_t(R) * kWarps * 8 + size_t(R) * 16 + 64;
+}
+
+template <typename T, bool CLUSTER>
+__global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
+  namespace cg = cooperative_groups;
+  using V = typename Vec<T>::type;
+  constexpr int VEC = Vec<T>::N;
+  const int G = A.G;
+  int rank, prob;
+  if constexpr (CLUSTER) {
+    rank = (int)cg::this_cluster().block_rank();
+    prob = (int)(blockIdx.x / G);
+  } else {
+    rank = (int)blockIdx.x;
+    prob = 0;
+  }
+  Ctl* ctl = A.ctl + prob;
+  const Params& prm = *A.prm;
+  if (ctl->done) return;  // uniform per problem
+  const long long m = A.m, n = A.n, ld = A.ld;
+  const int R = A.R;
+  T* Xg = static_cast<T*>(A.X) + prob * A.mat_stride;
+  const T* Cg = static_cast<const T*>(A.C) + prob * A.mat_stride;
+  double* phi = A.phi + prob * m;
+  double* av = A.a + prob * m;
+  double* rv = A.r + prob * m;
+  const double* pv = A.p + prob * m;
+  double* psi = A.psi + prob * n;
+  double* bv = A.b + prob * n;
+  double* sv = A.s + prob * n;
+  const double* qv = A.q + prob * n;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* Ct = reinterpret_cast<T*>(smem_raw);
+  T* Xt = Ct + (size_t)R * ld;
+  double* xrow = reinterpret_cast<double*>(Xt + (size_t)R * ld);  // n + 4
+  double* psi_s = xrow + n + 4;                                     // n
+  double* rowp = psi_s + n;                                         // R * kWarps
+  double* phi_s = rowp + (size_t)R * kWarps;                        // R
+  double* r_s = phi_s + R;                                          // R
+  __shared__ double red[kWarps];
+  __shared__ double bc[4];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long i0 = (long long)rank * R;
+  long long i1 = i0 + R;
+  if (i1 > m) i1 = m;
+  const int nr = i1 > i0 ? (int)(i1 - i0) : 0;
+  // column slice owned in the column phase
+  const long long j0 = n * rank / G, j1 = n * (rank + 1) / G;
+
+  auto xbuf = [&](int rk) -> double* {  // exchange row of CTA rk
+    if constexpr (CLUSTER) return cg::this_cluster().map_shared_rank(xrow, rk);
+    else return A.gscratch + (size_t)rk * (size_t)(n + 4);
+  };
+  auto xsync = [&]() {
+    if constexpr (CLUSTER) {
+      cg::this_cluster().sync();
+    } else {
+      grid_barrier(ctl);
+    }
+  };
+
+  // load the tiles (once per solve)
+  {
+    const long long elems = (long long)nr * ld;
+    const V* cs = reinterpret_cast<const V*>(Cg + i0 * ld);
+    const V* xs = reinterpret_cast<const V*>(Xg + i0 * ld);
+    V* cd = reinterpret_cast<V*>(Ct);
+    V* xd = reinterpret_cast<V*>(Xt);
+    for (long long t = threadIdx.x; t < elems / VEC; t += kThreads) {
+      cd[t] = cs[t];
+      xd[t] = xs[t];
+    }
+    for (long long j = threadIdx.x; j < n; j += kThreads) psi_s[j] = psi[j];
+    for (int t = threadIdx.x; t < nr; t += kThreads) phi_s[t] = phi[i0 + t];
+  }
+  __syncthreads();
+
+  const double rho = prm.rho, qd = prm.quad_d, qinv = prm.quad_inv;
+  const bool exact = sizeof(T) == 8;
+  const double dm = (double)m, dn = (double)n, mn = (double)(m + n);
+  long long k = ctl->k;
+  double theta = ctl->theta[k & 1];
+  double best = ctl->best;
+  long long last_imp = ctl->last_improvement;
+  const long long k0 = ctl->k0;
+  long long it = 0;
+
+  for (;;) {
+    // ---- 1. sweep own rows (thread: VEC consecutive columns; warp: 32*VEC)
+    for (int t = threadIdx.x; t < nr * kWarps; t += kThreads) rowp[t] = 0.0;
+    __syncthreads();
+    for (long long cw = (long long)warp * 32 * VEC; cw < ld; cw += (long long)kThreads * VEC) {
+      const long long cb = cw + (long long)lane * VEC;  // warp-uniform loop, per-lane validity
+      const bool ok = cb < ld;
+      double ps[VEC], cacc[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        ps[e] = (cb + e < n) ? psi_s[cb + e] : -INFINITY;
+        cacc[e] = 0.0;
+      }
+      for (int t = 0; t < nr; ++t) {
+        const double ph = phi_s[t];
+        double rs = 0.0;
+        if (ok) {
+          double x[VEC], c[VEC], o[VEC];
+          unpack(reinterpret_cast<const V*>(Xt + (size_t)t * ld)[cb / VEC], x);
+          unpack(reinterpret_cast<const V*>(Ct + (size_t)t * ld)[cb / VEC], c);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const double val = exact ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, c[e])), ph), ps[e])
+                                     : (fma(-rho, c[e], x[e]) + ph) + ps[e];
+            double nx = clamp0(val);
+            if (A.reg == REG_QUAD) nx = exact ? __ddiv_rn(nx, qd) : nx * qinv;
+            o[e] = nx;
+            cacc[e] += nx;
+            rs += nx;
+          }
+          reinterpret_cast<V*>(Xt + (size_t)t * ld)[cb / VEC] = pack<T>(o);
+        }
+        rs = warp_sum(rs);
+        if (lane == 0) rowp[t * kWarps + warp] += rs;
+      }
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        if (cb + e < n) xrow[cb + e] = cacc[e];
+    }
+    __syncthreads();
+    // row sums -> r (own rows), scalar partials
+    double sr = 0.0, sr2 = 0.0, sR = 0.0;
+    for (int t = threadIdx.x; t < nr; t += kThreads) {
+      double Rr = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) Rr += rowp[t * kWarps + w];
+      const double ri = Rr - pv[i0 + t];
+      r_s[t] = ri;
+      sr += ri;
+      sr2 += ri * ri;
+      sR += Rr;
+    }
+    {
+      const double t1 = block_sum(sr, red);
+      const double t2 = block_sum(sr2, red);
+      const double t3 = block_sum(sR, red);
+      if (threadIdx.x == 0) {
+        if constexpr (CLUSTER) {
+          xrow[n] = t1;
+          xrow[n + 1] = t2;
+          xrow[n + 2] = t3;
+        } else {
+          double* g = xbuf(rank);
+          g[n] = t1;
+          g[n + 1] = t2;
+          g[n + 2] = t3;
+        }
+      }
+      if constexpr (!CLUSTER) {
+        double* g = xbuf(rank);
+        for (long long j = threadIdx.x; j < n; j += kThreads) g[j] = xrow[j];
+      }
+    }
+    xsync();  // ---- 2. column partials and scalar partials visible
+    if (threadIdx.x == 0) {
+      double u1 = 0.0, u2 = 0.0;
+      for (int h = 0; h < G; ++h) {
+        const double* g = xbuf(h);
+        u1 += g[n];
+        u2 += g[n + 1];
+      }
+      bc[0] = u1;
+      bc[1] = u2;
+    }
+    __syncthreads();
+    const double eta = __ddiv_rn(bc[0], mn);
+    const double shift = __dsub_rn(2.0 * eta, theta);
+    const double rsq = bc[1];
+    // ---- 3. own rows: phi, a; owned columns: s, psi, b
+    for (int t = threadIdx.x; t < nr; t += kThreads) {
+      const double ri = r_s[t], ai = av[i0 + t];
+      const double ph = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift), dn);
+      phi_s[t] = ph;
+      av[i0 + t] = __dsub_rn(ai, ri);
+    }
+    double ssq = 0.0;
+    for (long long j = j0 + threadIdx.x; j < j1; j += kThreads) {
+      double S = 0.0;
+      for (int h = 0; h < G; ++h) S += xbuf(h)[j];
+      const double sj = __dsub_rn(S, qv[j]);
+      const double bj = bv[j];
+      sv[j] = sj;
+      psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift), dm);
+      bv[j] = __dsub_rn(bj, sj);
+      ssq += sj * sj;
+    }
+    {
+      const double t4 = block_sum(ssq, red);
+      if constexpr (CLUSTER) xsync();  // peers done reading this CTA's column partials
+      if (threadIdx.x == 0) {
+        if constexpr (CLUSTER) xrow[n + 3] = t4;
+        else xbuf(rank)[n + 3] = t4;
+      }
+      if constexpr (CLUSTER) {  // publish owned psi slice in smem for peers
+        for (long long j = j0 + threadIdx.x; j < j1; j += kThreads) xrow[j] = psi[j];
+      }
+    }
+    xsync();  // ---- 4. psi slices and sum s^2 partials visible
+    if constexpr (CLUSTER) {
+      for (int h = 0; h < G; ++h) {
+        const long long a0 = n * h / G, a1 = n * (h + 1) / G;
+        const double* g = xbuf(h);
+        for (long long j = a0 + threadIdx.x; j < a1; j += kThreads) psi_s[j] = g[j];
+      }
+    } else {
+      for (long long j = threadIdx.x; j < n; j += kThreads) psi_s[j] = __ldcg(psi + j);
+    }
+    if (threadIdx.x == 0) {
+      double u4 = 0.0;
+      for (int h = 0; h < G; ++h) u4 += xbuf(h)[n + 3];
+      bc[2] = u4;
+    }
+    __syncthreads();
+    const double nr2 = sqrt(rsq), ns2 = sqrt(bc[2]);
+    const double rp = (nr2 < ns2) ? ns2 : nr2;
+    theta = __dsub_rn(theta, eta);
+    ++k;
+    ++it;
+    const long long kk = k - k0;
+    bool done = false;
+    int term = TERM_MAXITER;
+    if (prm.solving) {
+      if (!(rp - rp == 0.0)) {
+        done = true;
+        term = TERM_NONFINITE;
+      } else {
+        if (rp < best * (1.0 - 1e-14)) {
+          best = rp;
+          last_imp = kk;
+        }
+        const bool at_check = (kk % prm.check_every) == 0;
+        if (at_check && rp <= prm.tol_primal) {
+          done = true;
+          term = TERM_CONVERGED;
+        } else if (kk - last_imp >= 10000) {
+          done = true;
+          term = TERM_STALLED;
+        } else if (kk >= prm.max_iter) {
+          done = true;
+          term = TERM_MAXITER;
+        }
+      }
+    } else if (it >= A.iters) {
+      done = true;
+    }
+    if (done) {
+      if (rank == 0 && threadIdx.x == 0) {
+        ctl->k = k;
+        ctl->theta[k & 1] = theta;
+        ctl->eta = eta;
+        ctl->r_primal = rp;
+        ctl->best = best;
+        ctl->last_improvement = last_imp;
+        if (prm.solving) {
+          ctl->done = 1;
+          ctl->termination = term;
+        }
+      }
+      break;
+    }
+    if constexpr (CLUSTER) {
+      // peers may still read this CTA's psi slice / partials before the next
+      // iteration overwrites xrow
+      cg::this_cluster().sync();
+    }
+  }
+  // write back the plan, phi and r of own rows (psi, s, b, a already global)
+  {
+    const long long elems = (long long)nr * ld;
+    V* xd = reinterpret_cast<V*>(Xg + i0 * ld);
+    const V* xs = reinterpret_cast<const V*>(Xt);
+    for (long long t = threadIdx.x; t < elems / VEC; t += kThreads) xd[t] = xs[t];
+    for (int t = threadIdx.x; t < nr; t += kThreads) {
+      phi[i0 + t] = phi_s[t];
+      rv[i0 + t] = r_s[t];
+    }
+  }
+  if constexpr (CLUSTER) cg::this_cluster().sync();  // no CTA exits while peers read its smem
+}
+
+}  // namespace otdrk
