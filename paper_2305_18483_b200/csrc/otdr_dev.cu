@@ -1208,8 +1208,10 @@ otdr_status otdr_dev_solve(otdr_dev* ctx, const otdr_solve_opts* o, otdr_solve_r
       ctx->h_ctl->fused_shifted = 0;
       ctx->push_ctl();
     }
-    ctx->launch_cert(1, 0, 0);
-    ctx->check_launch();
+    if (!resident) {  // the resident kernel already evaluated the objective on chip
+      ctx->launch_cert(1, 0, 0);
+      ctx->check_launch();
+    }
     ctx->pull_ctl();
     res->iterations = ctx->h_ctl->k;
     res->termination = ctx->h_ctl->termination;

@@ -105,6 +105,16 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
     if constexpr (CLUSTER) return cg::this_cluster().map_shared_rank(xrow, rk);
     else return A.gscratch + (size_t)rk * (size_t)(n + 4);
   };
+  auto xget = [&](int rk, long long idx) -> double {  // peer read (L2 in grid mode)
+    if constexpr (CLUSTER) return xbuf(rk)[idx];
+    else return __ldcg(xbuf(rk) + idx);
+  };
+  // fixed-order fold of one exchange slot over the G CTAs by one warp
+  auto warp_fold = [&](long long idx) -> double {
+    double s = 0.0;
+    for (int h = lane; h < G; h += 32) s += xget(h, idx);
+    return warp_sum(s);
+  };
   auto xsync = [&]() {
     if constexpr (CLUSTER) {
       cg::this_cluster().sync();
@@ -213,15 +223,9 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
       }
     }
     xsync();  // ---- 2. column partials and scalar partials visible
-    if (threadIdx.x == 0) {
-      double u1 = 0.0, u2 = 0.0;
-      for (int h = 0; h < G; ++h) {
-        const double* g = xbuf(h);
-        u1 += g[n];
-        u2 += g[n + 1];
-      }
-      bc[0] = u1;
-      bc[1] = u2;
+    if (warp < 2) {
+      const double u = warp_fold(n + warp);
+      if (lane == 0) bc[warp] = u;
     }
     __syncthreads();
     const double eta = __ddiv_rn(bc[0], mn);
@@ -234,16 +238,17 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
       phi_s[t] = ph;
       av[i0 + t] = __dsub_rn(ai, ri);
     }
-    double ssq = 0.0;
-    for (long long j = j0 + threadIdx.x; j < j1; j += kThreads) {
-      double S = 0.0;
-      for (int h = 0; h < G; ++h) S += xbuf(h)[j];
-      const double sj = __dsub_rn(S, qv[j]);
-      const double bj = bv[j];
-      sv[j] = sj;
-      psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift), dm);
-      bv[j] = __dsub_rn(bj, sj);
-      ssq += sj * sj;
+    double ssq = 0.0;  // warp per owned column: lanes fold the G partials
+    for (long long j = j0 + warp; j < j1; j += kWarps) {
+      const double S = warp_fold(j);
+      if (lane == 0) {
+        const double sj = __dsub_rn(S, qv[j]);
+        const double bj = bv[j];
+        sv[j] = sj;
+        psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift), dm);
+        bv[j] = __dsub_rn(bj, sj);
+        ssq += sj * sj;
+      }
     }
     {
       const double t4 = block_sum(ssq, red);
@@ -266,10 +271,9 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
     } else {
       for (long long j = threadIdx.x; j < n; j += kThreads) psi_s[j] = __ldcg(psi + j);
     }
-    if (threadIdx.x == 0) {
-      double u4 = 0.0;
-      for (int h = 0; h < G; ++h) u4 += xbuf(h)[n + 3];
-      bc[2] = u4;
+    if (warp == 0) {
+      const double u4 = warp_fold(n + 3);
+      if (lane == 0) bc[2] = u4;
     }
     __syncthreads();
     const double nr2 = sqrt(rsq), ns2 = sqrt(bc[2]);
@@ -323,6 +327,28 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
       // peers may still read this CTA's psi slice / partials before the next
       // iteration overwrites xrow
       cg::this_cluster().sync();
+    }
+  }
+  // primal objective <C,X> + h(X) (problem.cpp:76-85) from the resident tiles
+  {
+    double lin = 0.0, xsq = 0.0;
+    const long long elems = (long long)nr * ld;
+    for (long long t = threadIdx.x; t < elems; t += kThreads) {
+      const double xv = (double)Xt[t], cv = (double)Ct[t];
+      lin += cv * xv;
+      xsq += xv * xv;
+    }
+    const double t1 = block_sum(lin, red);
+    const double t2 = block_sum(xsq, red);
+    if (threadIdx.x == 0) {
+      double* g = CLUSTER ? xrow : xbuf(rank);
+      g[n] = t1;
+      g[n + 1] = t2;
+    }
+    xsync();
+    if (rank == 0 && warp == 0) {
+      const double u1 = warp_fold(n), u2 = warp_fold(n + 1);
+      if (lane == 0) ctl->objective = u1 + (A.reg == REG_QUAD ? 0.5 * prm.alpha * u2 : 0.0);
     }
   }
   // write back the plan, phi and r of own rows (psi, s, b, a already global)

@@ -412,3 +412,34 @@ def test_gl_fused_and_trace_match_unfused(ora):
                   max_iter=301, tol_primal=1e-300, record_trace=True, check_every=50, deterministic=True)
     assert [r.support for r in c.trace] == [r[4] for r in o.trace]
     assert c.support_last_change == o.support_last_change
+
+
+@pytest.mark.parametrize("storage", ["f64", "f32"])
+@pytest.mark.parametrize("m,n,kind", [(20, 20, "none"), (300, 517, "quad"), (1000, 1000, "quad"),
+                                      (5, 3000, "none"), (1500, 1400, "quad")])
+def test_resident_matches_streaming(ora, monkeypatch, storage, m, n, kind):
+    """The on-chip resident loop (grid mode) and the streaming graph loop give
+    the same trajectory (same element-wise arithmetic; reduction order only)."""
+    C, p, q, *_ = ora.gaussian_problem(m, n, 2)
+    reg = otdr.QuadraticReg(5e-3 * (m + n)) if kind == "quad" else otdr.ZeroReg()
+    out = {}
+    for mode in ("on", "off"):
+        monkeypatch.setenv("OTDR_RESIDENT", mode)
+        eng = otdr.Engine(m, n, storage)
+        eng.set_problem(C, p, q)
+        eng.set_regularizer(reg)
+        eng.set_state()
+        eng.step(otdr.default_stepsize(m, n), 37)
+        st = eng.get_state()
+        eng.set_state()
+        rep = eng.solve(otdr.SolverOptions(tol_primal=1e-6, max_iter=5000, storage=storage), with_state=True)
+        out[mode] = (st, rep)
+        eng.close()
+    a, b = out["on"], out["off"]
+    tol = 1e-12 if storage == "f64" else 1e-6
+    assert a[0].k == b[0].k == 37
+    assert rel(a[0].X, b[0].X) <= tol and rel(a[0].phi, b[0].phi) <= tol and rel(a[0].psi, b[0].psi) <= tol
+    assert abs(a[0].theta - b[0].theta) <= 1e-12 * max(1, abs(b[0].theta))
+    assert a[1].termination == b[1].termination
+    assert abs(a[1].iterations - b[1].iterations) <= (0 if storage == "f64" else 2)
+    assert abs(a[1].objective - b[1].objective) <= 1e-9 * abs(b[1].objective)
