@@ -180,6 +180,33 @@ otdr_status otdr_dev_time_steps(otdr_dev* ctx, double rho, int64_t iters, double
 /* Number of kernel launches one DR iteration issues (sweep, reduce, update). */
 int otdr_dev_kernels_per_iteration(const otdr_dev* ctx);
 
+/* ---------------------------------------------------------------- batched
+ * B independent problems of one shape solved by ONE launch, each problem owned
+ * by a thread-block cluster that keeps its C and X in (distributed) shared
+ * memory for the whole solve. Equivalent to B sequential solve() calls from
+ * default_init (solver.cpp:104-241) -- the GAN minibatch loop of the paper
+ * (ot_cost_gradient, duality.cpp:26-31). Zero / quadratic
+ * regularizers; shapes whose per-problem tiles exceed a 16-CTA cluster return
+ * OTDR_E_UNSUPPORTED (callers then run per-problem contexts). */
+typedef struct otdr_batch otdr_batch;
+otdr_status otdr_batch_create(int device, otdr_storage storage, int64_t batch, int64_t m,
+                              int64_t n, otdr_batch** out);
+void otdr_batch_destroy(otdr_batch* bt);
+const char* otdr_batch_last_error(const otdr_batch* bt);
+/* costs B x m x n, p B x m, q B x n (each problem validated by the caller). */
+otdr_status otdr_batch_set_problems(otdr_batch* bt, const double* costs, const double* p,
+                                    const double* q);
+/* per-problem squared-distance costs normalised by their own max
+ * (gaussian_problem per seed): src B x m x d, tgt B x n x d. */
+otdr_status otdr_batch_build_sqdist_costs(otdr_batch* bt, const double* src, const double* tgt,
+                                          int d, const double* p, const double* q);
+otdr_status otdr_batch_set_regularizer(otdr_batch* bt, otdr_reg_kind kind, double alpha);
+/* results: B entries. opts->fused / record_trace / has_tol_gap unsupported. */
+otdr_status otdr_batch_solve(otdr_batch* bt, const otdr_solve_opts* opts,
+                             otdr_solve_result* results);
+/* any pointer may be NULL: X B x m x n, phi B x m, psi B x n. */
+otdr_status otdr_batch_get_plans(otdr_batch* bt, double* X, double* phi, double* psi);
+
 #ifdef __cplusplus
 }
 #endif

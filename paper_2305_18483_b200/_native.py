@@ -67,6 +67,9 @@ EXPORTS = [
     "otdr_dev_solve", "otdr_dev_get_state", "otdr_dev_objective", "otdr_dev_duality_gap",
     "otdr_dev_get_trace", "otdr_dev_profile", "otdr_dev_time_steps",
     "otdr_dev_kernels_per_iteration",
+    "otdr_batch_create", "otdr_batch_destroy", "otdr_batch_last_error", "otdr_batch_set_problems",
+    "otdr_batch_build_sqdist_costs", "otdr_batch_set_regularizer", "otdr_batch_solve",
+    "otdr_batch_get_plans",
     # include/otdr_datagen.h
     "otdr_gaussian_points", "otdr_adaptation_points", "otdr_dev_nccl_unique_id",
 ]
@@ -111,6 +114,17 @@ def lib():
     L.otdr_adaptation_points.argtypes = [ct.c_int64, ct.c_int64, ct.c_int, ct.c_uint64, ct.c_int,
                                          _dp, _dp, _i32p, _i32p]
     L.otdr_dev_nccl_unique_id.argtypes = [ct.c_char_p]
+    L.otdr_batch_create.argtypes = [ct.c_int, ct.c_int, ct.c_int64, ct.c_int64, ct.c_int64,
+                                    ct.POINTER(vp)]
+    L.otdr_batch_destroy.argtypes = [vp]
+    L.otdr_batch_destroy.restype = None
+    L.otdr_batch_last_error.argtypes = [vp]
+    L.otdr_batch_last_error.restype = ct.c_char_p
+    L.otdr_batch_set_problems.argtypes = [vp, _dp, _dp, _dp]
+    L.otdr_batch_build_sqdist_costs.argtypes = [vp, _dp, _dp, ct.c_int, _dp, _dp]
+    L.otdr_batch_set_regularizer.argtypes = [vp, ct.c_int, ct.c_double]
+    L.otdr_batch_solve.argtypes = [vp, ct.POINTER(SolveOpts), ct.POINTER(SolveResult)]
+    L.otdr_batch_get_plans.argtypes = [vp, _dp, _dp, _dp]
     L.otdr_dev_kernels_per_iteration.argtypes = [vp]
     L.otdr_dev_kernels_per_iteration.restype = ct.c_int
     _lib = L

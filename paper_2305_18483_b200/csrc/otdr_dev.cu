@@ -1312,3 +1312,5 @@ otdr_status otdr_dev_get_trace(otdr_dev* ctx, otdr_trace_row* rows, int64_t cap,
 }
 
 }  // extern "C"
+
+#include "otdr_batch.cuh"

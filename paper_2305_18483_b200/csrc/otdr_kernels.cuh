@@ -73,8 +73,11 @@ struct Ctl {
   unsigned long long t0_ns;
   double objective, gap, dual_value, dres;
   long long last_support;
-  unsigned int bar_count;  // grid barrier of the cooperative finalize kernel
-  unsigned int bar_gen;
+  // Monotonic 64-bit arrival counters of the software grid barriers; each is
+  // used by exactly one kernel with a fixed grid size, so between launches it
+  // always holds a multiple of that grid size.
+  unsigned long long bar_fin;  // cooperative finalize kernel
+  unsigned long long bar_res;  // resident solve kernel
 };
 
 struct TraceRow {
@@ -907,19 +910,16 @@ struct FinalizeArgs {
   int cert_follows;
 };
 
-__device__ __forceinline__ void grid_barrier(Ctl* ctl) {
+__device__ __forceinline__ void grid_barrier(unsigned long long* counter) {
+  // Arrival number a belongs to generation a / gridDim.x; wait until the
+  // counter reaches the end of that generation (one atomic + one polled word).
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned int* gen = &ctl->bar_gen;
-    const unsigned int g = *gen;
     __threadfence();
-    if (atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1) {
-      ctl->bar_count = 0;
-      __threadfence();
-      atomicAdd(&ctl->bar_gen, 1u);
-    } else {
-      while (*gen == g) {
-      }
+    const unsigned long long arrived = atomicAdd(counter, 1ull);
+    const unsigned long long target = (arrived / gridDim.x + 1ull) * gridDim.x;
+    volatile unsigned long long* cnt = counter;
+    while (*cnt < target) {
     }
     __threadfence();
   }
@@ -969,7 +969,7 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinalizeArgs a) {
     a.part[blockIdx.x * 3 + 1] = t2;
     a.part[blockIdx.x * 3 + 2] = t3;
   }
-  grid_barrier(ctl);
+  grid_barrier(&ctl->bar_fin);
   if (threadIdx.x == 0) {
     double u1 = 0.0, u2 = 0.0, u3 = 0.0;
     for (unsigned c = 0; c < gridDim.x; ++c) {

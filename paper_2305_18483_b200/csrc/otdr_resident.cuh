@@ -109,17 +109,25 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
     if constexpr (CLUSTER) return xbuf(rk)[idx];
     else return __ldcg(xbuf(rk) + idx);
   };
-  // fixed-order fold of one exchange slot over the G CTAs by one warp
+  // fixed-order fold of one exchange slot over the G (<= 160) CTAs by one
+  // warp: all peer loads are issued before any add (one L2 round trip)
   auto warp_fold = [&](long long idx) -> double {
+    double v[5];
+#pragma unroll
+    for (int u = 0; u < 5; ++u) {
+      const int h = lane + 32 * u;
+      v[u] = h < G ? xget(h, idx) : 0.0;
+    }
     double s = 0.0;
-    for (int h = lane; h < G; h += 32) s += xget(h, idx);
+#pragma unroll
+    for (int u = 0; u < 5; ++u) s += v[u];
     return warp_sum(s);
   };
   auto xsync = [&]() {
     if constexpr (CLUSTER) {
       cg::this_cluster().sync();
     } else {
-      grid_barrier(ctl);
+      grid_barrier(&ctl->bar_res);
     }
   };
 

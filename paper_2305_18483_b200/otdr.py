@@ -577,6 +577,106 @@ class Engine:
         return self._L.otdr_dev_kernels_per_iteration(self._h)
 
 
+class BatchEngine:
+    """B same-shape problems solved by one launch (libotdr_dev.so otdr_batch_*):
+    each problem's C and X stay resident in a thread-block cluster's shared
+    memory for the whole solve. Equivalent to B sequential `solve()` calls from
+    `default_init` -- the GAN minibatch loop of the paper."""
+
+    def __init__(self, batch: int, m: int, n: int, storage: str = "f32", device: int = 0):
+        self._L = nat.lib()
+        self.batch, self.m, self.n, self.storage = batch, m, n, storage
+        h = ct.c_void_p()
+        rc = self._L.otdr_batch_create(device, _STORAGE[storage], batch, m, n, ct.byref(h))
+        if rc != nat.OTDR_OK:
+            raise _ERRORS.get(rc, DeviceError)(
+                f"otdr_batch_create failed ({nat.STATUS_NAMES.get(rc, rc)})")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.otdr_batch_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ck(self, rc: int):
+        if rc != nat.OTDR_OK:
+            msg = self._L.otdr_batch_last_error(self._h).decode(errors="replace")
+            raise _ERRORS.get(rc, DeviceError)(msg or nat.STATUS_NAMES.get(rc, str(rc)))
+
+    def set_problems(self, costs, p, q):
+        B, m, n = self.batch, self.m, self.n
+        C = _f64(costs, (B, m, n))
+        self._ck(self._L.otdr_batch_set_problems(self._h, nat.dptr(C), nat.dptr(_f64(p, (B, m))),
+                                                 nat.dptr(_f64(q, (B, n)))))
+
+    def build_sqdist_costs(self, src, tgt, p, q):
+        B, m, n = self.batch, self.m, self.n
+        s = _f64(src)
+        t = _f64(tgt)
+        if s.shape[:2] != (B, m) or t.shape[:2] != (B, n) or s.shape[2] != t.shape[2]:
+            raise DimensionMismatch("point clouds do not match the batch shape")
+        self._ck(self._L.otdr_batch_build_sqdist_costs(self._h, nat.dptr(s), nat.dptr(t), s.shape[2],
+                                                       nat.dptr(_f64(p, (B, m))),
+                                                       nat.dptr(_f64(q, (B, n)))))
+
+    def set_regularizer(self, reg: Regularizer):
+        if not isinstance(reg, (ZeroReg, QuadraticReg)):
+            raise Unsupported("the batched entry point covers zero / quadratic regularizers")
+        self._ck(self._L.otdr_batch_set_regularizer(self._h, reg.kind, reg.param))
+
+    def solve(self, opt: SolverOptions) -> list:
+        o = nat.SolveOpts(opt.rho, int(opt.max_iter), opt.tol_primal, int(opt.tol_gap is not None),
+                          0.0 if opt.tol_gap is None else float(opt.tol_gap), int(opt.check_every),
+                          int(bool(opt.deterministic)), int(bool(opt.record_trace)),
+                          int(bool(opt.fused)))
+        res = (nat.SolveResult * self.batch)()
+        self._ck(self._L.otdr_batch_solve(self._h, ct.byref(o), res))
+        return [SolveReport(None, r.objective, r.iterations, Termination(r.termination), r.rho,
+                            r.r_primal, [], -1, r.device_ms) for r in res]
+
+    def plans(self):
+        B, m, n = self.batch, self.m, self.n
+        X = np.empty((B, m, n))
+        phi = np.empty((B, m))
+        psi = np.empty((B, n))
+        self._ck(self._L.otdr_batch_get_plans(self._h, nat.dptr(X), nat.dptr(phi), nat.dptr(psi)))
+        return X, phi, psi
+
+
+def solve_batch(problems, reg: Regularizer, options: Optional[SolverOptions] = None) -> list:
+    """`[solve(pr, reg, options) for pr in problems]` for same-shape problems,
+    in one device launch; shapes beyond a cluster fall back to per-problem
+    device solves (still on the GPU)."""
+    opt = options or SolverOptions()
+    if not problems:
+        return []
+    if opt.init is not None or opt.tol_gap is not None or opt.record_trace or opt.fused:
+        return [solve(pr, reg, opt) for pr in problems]
+    m, n = problems[0].rows(), problems[0].cols()
+    if any(pr.cost.shape != (m, n) for pr in problems):
+        raise DimensionMismatch("solve_batch needs problems of one shape")
+    try:
+        be = BatchEngine(len(problems), m, n, opt.storage, opt.device)
+    except Unsupported:
+        return [solve(pr, reg, opt) for pr in problems]
+    be.set_problems(np.stack([pr.cost for pr in problems]), np.stack([pr.p for pr in problems]),
+                    np.stack([pr.q for pr in problems]))
+    be.set_regularizer(reg)
+    reps = be.solve(opt)
+    X, phi, psi = be.plans()
+    for b, rep in enumerate(reps):
+        rep.state = SolverState(X[b], phi[b], psi[b], None, None, float("nan"), None, None,
+                                float("nan"), rep.iterations)
+    be.close()
+    return reps
+
+
 def _engine_for(problem: Problem, storage: str, device: int) -> Engine:
     key = (storage, device)
     eng = problem._engines.get(key)

@@ -442,4 +442,45 @@ def test_resident_matches_streaming(ora, monkeypatch, storage, m, n, kind):
     assert abs(a[0].theta - b[0].theta) <= 1e-12 * max(1, abs(b[0].theta))
     assert a[1].termination == b[1].termination
     assert abs(a[1].iterations - b[1].iterations) <= (0 if storage == "f64" else 2)
-    assert abs(a[1].objective - b[1].objective) <= 1e-9 * abs(b[1].objective)
+    assert abs(a[1].objective - b[1].objective) <= (1e-9 if storage == "f64" else 1e-6) * abs(b[1].objective)
+
+
+@pytest.mark.parametrize("storage", ["f64", "f32"])
+def test_batched_solve_matches_sequential(ora, storage):
+    """cfg5 shape at reduced batch: one cluster-resident launch == B solve()s."""
+    B, m = 6, 96
+    probs = [ora.gaussian_problem(m, m, b) for b in range(B)]
+    alpha = 5e-3 * 2 * m
+    reps = otdr.solve_batch([otdr.Problem(C, p, q) for (C, p, q, *_) in probs], otdr.QuadraticReg(alpha),
+                            otdr.SolverOptions(tol_primal=1e-6, max_iter=20000, storage=storage))
+    for (C, p, q, *_), rep in zip(probs, reps):
+        Co = C if storage == "f64" else C.astype(np.float32).astype(np.float64)
+        o = ora.solve(ora.Problem(Co, p, q), ora.quad_reg(alpha), tol_primal=1e-6, max_iter=20000)
+        assert rep.termination.name == o.termination == "Converged"
+        assert abs(rep.iterations - o.iterations) <= (1 if storage == "f64" else 3)
+        assert abs(rep.objective - o.objective) <= 1e-6 * abs(o.objective)
+        assert rel(rep.plan(), o.state.X) <= (1e-7 if storage == "f64" else 1e-4)
+
+
+def test_batched_device_cost_and_512(ora):
+    """512 x 512 per problem (the cfg5 tile): device-built costs, B = 3."""
+    B, m = 3, 512
+    src = np.empty((B, m, 2))
+    tgt = np.empty((B, m, 2))
+    ps = np.full((B, m), 1.0 / m)
+    refs = []
+    for b in range(B):
+        C, p, q, s, t = ora.gaussian_problem(m, m, b)
+        src[b], tgt[b] = s, t
+        refs.append((C, p, q))
+    be = otdr.BatchEngine(B, m, m, "f32")
+    be.build_sqdist_costs(src, tgt, ps, ps)
+    be.set_regularizer(otdr.QuadraticReg(5.12))
+    reps = be.solve(otdr.SolverOptions(tol_primal=1e-4, max_iter=20000))
+    X, phi, psi = be.plans()
+    for b, (C, p, q) in enumerate(refs):
+        o = ora.solve(ora.Problem(C.astype(np.float32).astype(np.float64), p, q), ora.quad_reg(5.12),
+                      tol_primal=1e-4, max_iter=20000)
+        assert reps[b].termination.name == "Converged"
+        assert abs(reps[b].iterations - o.iterations) <= 3
+        assert abs(reps[b].objective - o.objective) <= 1e-6 * abs(o.objective)
