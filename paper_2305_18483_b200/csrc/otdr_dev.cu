@@ -453,8 +453,8 @@ struct otdr_dev {
     }
   }
 
-  // TMA tile plan: column stripes of 512 B (else 256 B) per box row, R <= 256
-  // rows per CTA (TMA box limit), a cluster of K <= 16 CTAs per class
+  // TMA tile plan: column stripes of 256 B (else 512 B) per box row, R <= 256
+  // rows per CTA (TMA box limit), a cluster of K <= 8 CTAs per class
   // segment, <= ~72 KB of tiles per CTA so three CTAs share an SM.
   void plan_gl_cluster() {
     glc_tn = 0;
@@ -476,13 +476,13 @@ struct otdr_dev {
       std::sscanf(ev, "%d,%d,%d", &kb, &kmin, &force_row_bytes);
       tile_budget = size_t(kb) * 1024;
     }
-    for (int row_bytes : {512, 256}) {
+    for (int row_bytes : {256, 512}) {  // 256-B rows with K <= 8 measured fastest
       if (force_row_bytes && row_bytes != force_row_bytes) continue;
       const int tn = int(row_bytes / esz);
       const long long rows_max =
           std::min<long long>(256, (long long)(tile_budget / (2 * size_t(row_bytes))));
       int k = std::max(1, kmin);
-      while (k < 16 && (lmax + k - 1) / k > rows_max) k *= 2;
+      while (k < 8 && (lmax + k - 1) / k > rows_max) k *= 2;
       const long long rows = (lmax + k - 1) / k;
       if (rows > rows_max) continue;
       glc_tn = tn;

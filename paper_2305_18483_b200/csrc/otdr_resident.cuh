@@ -46,10 +46,18 @@ struct ResidentArgs {
 // Shared-memory layout (dynamic): C tile [R][ld] T | X tile [R][ld] T |
 // xrow: this CTA's exchange row [n + 4] doubles (column sums | sr | sr2 | sR | ssq)
 // | psi_s [n] | rowp [R][kWarps] | phi_s [R] | r_s [R]
+// Warps split into column chunks (32 lanes x VEC columns) x row subsets.
+template <typename T>
+__host__ __device__ inline int resident_row_sets(long long ld) {
+  const long long nch = (ld + 32 * Vec<T>::N - 1) / (32 * Vec<T>::N);
+  return nch >= kWarps ? 1 : (int)(kWarps / nch);
+}
+
 template <typename T>
 __host__ __device__ inline size_t resident_smem_bytes(long long R, long long n, long long ld) {
+  const int sets = resident_row_sets<T>(ld);
   return size_t(2 * R * ld) * sizeof(T) + size_t(n + 4) * 8 + size_t(n) * 8 +
-         size_t(R) * kWarps * 8 + size_t(R) * 16 + 64;
+         size_t(R) * kWarps * 8 + size_t(R) * 16 + (sets > 1 ? size_t(sets) * ld * 8 : 0) + 64;
 }
 
 template <typename T, bool CLUSTER>
@@ -90,6 +98,9 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
   double* rowp = psi_s + n;                                         // R * kWarps
   double* phi_s = rowp + (size_t)R * kWarps;                        // R
   double* r_s = phi_s + R;                                          // R
+  double* colbuf = r_s + R;                                         // sets x ld (sets > 1)
+  const int nsets = resident_row_sets<T>(ld);
+  const long long nch = (ld + 32 * VEC - 1) / (32 * VEC);
   __shared__ double red[kWarps];
   __shared__ double bc[4];
 
@@ -161,8 +172,11 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
     // ---- 1. sweep own rows (thread: VEC consecutive columns; warp: 32*VEC)
     for (int t = threadIdx.x; t < nr * kWarps; t += kThreads) rowp[t] = 0.0;
     __syncthreads();
-    for (long long cw = (long long)warp * 32 * VEC; cw < ld; cw += (long long)kThreads * VEC) {
-      const long long cb = cw + (long long)lane * VEC;  // warp-uniform loop, per-lane validity
+    // Warp w: column chunks c = w % nch (+kWarps...) and rows set, set+nsets, ...
+    const int wset = (nsets > 1) ? warp / (int)nch : 0;
+    const bool wactive = (nsets > 1) ? (warp < (int)nch * nsets) : true;
+    for (long long c = (nsets > 1) ? warp % nch : warp; wactive && c < nch; c += (nsets > 1) ? nch : kWarps) {
+      const long long cb = c * 32 * VEC + (long long)lane * VEC;
       const bool ok = cb < ld;
       double ps[VEC], cacc[VEC];
 #pragma unroll
@@ -170,31 +184,54 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
         ps[e] = (cb + e < n) ? psi_s[cb + e] : -INFINITY;
         cacc[e] = 0.0;
       }
-      for (int t = 0; t < nr; ++t) {
-        const double ph = phi_s[t];
-        double rs = 0.0;
-        if (ok) {
-          double x[VEC], c[VEC], o[VEC];
-          unpack(reinterpret_cast<const V*>(Xt + (size_t)t * ld)[cb / VEC], x);
-          unpack(reinterpret_cast<const V*>(Ct + (size_t)t * ld)[cb / VEC], c);
+      // two rows per step: independent shuffle chains overlap
+      for (int t = wset; t < nr; t += 2 * nsets) {
+        const int t2 = t + nsets;
+        const bool has2 = t2 < nr;
+        double rs[2] = {0.0, 0.0};
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            const double val = exact ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, c[e])), ph), ps[e])
-                                     : (fma(-rho, c[e], x[e]) + ph) + ps[e];
-            double nx = clamp0(val);
-            if (A.reg == REG_QUAD) nx = exact ? __ddiv_rn(nx, qd) : nx * qinv;
-            o[e] = nx;
-            cacc[e] += nx;
-            rs += nx;
+        for (int u = 0; u < 2; ++u) {
+          const int tt = u ? t2 : t;
+          if (ok && (u == 0 || has2)) {
+            const double ph = phi_s[tt];
+            double x[VEC], cc[VEC], o[VEC];
+            unpack(reinterpret_cast<const V*>(Xt + (size_t)tt * ld)[cb / VEC], x);
+            unpack(reinterpret_cast<const V*>(Ct + (size_t)tt * ld)[cb / VEC], cc);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+              const double val = exact ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, cc[e])), ph), ps[e])
+                                       : (fma(-rho, cc[e], x[e]) + ph) + ps[e];
+              double nx = clamp0(val);
+              if (A.reg == REG_QUAD) nx = exact ? __ddiv_rn(nx, qd) : nx * qinv;
+              o[e] = nx;
+              cacc[e] += nx;
+              rs[u] += nx;
+            }
+            reinterpret_cast<V*>(Xt + (size_t)tt * ld)[cb / VEC] = pack<T>(o);
           }
-          reinterpret_cast<V*>(Xt + (size_t)t * ld)[cb / VEC] = pack<T>(o);
         }
-        rs = warp_sum(rs);
-        if (lane == 0) rowp[t * kWarps + warp] += rs;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          rs[0] += __shfl_xor_sync(0xffffffffu, rs[0], o);
+          rs[1] += __shfl_xor_sync(0xffffffffu, rs[1], o);
+        }
+        if (lane == 0) {
+          rowp[t * kWarps + warp] += rs[0];
+          if (has2) rowp[t2 * kWarps + warp] += rs[1];
+        }
       }
+      double* cdst = (nsets > 1) ? colbuf + (size_t)wset * ld : xrow;
 #pragma unroll
       for (int e = 0; e < VEC; ++e)
-        if (cb + e < n) xrow[cb + e] = cacc[e];
+        if (cb + e < ((nsets > 1) ? ld : n)) cdst[cb + e] = cacc[e];
+    }
+    if (nsets > 1) {  // fold the row subsets' column partials in a fixed order
+      __syncthreads();
+      for (long long j = threadIdx.x; j < n; j += kThreads) {
+        double sacc = 0.0;
+        for (int w = 0; w < nsets; ++w) sacc += colbuf[(size_t)w * ld + j];
+        xrow[j] = sacc;
+      }
     }
     __syncthreads();
     // row sums -> r (own rows), scalar partials
@@ -271,10 +308,11 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
     }
     xsync();  // ---- 4. psi slices and sum s^2 partials visible
     if constexpr (CLUSTER) {
-      for (int h = 0; h < G; ++h) {
-        const long long a0 = n * h / G, a1 = n * (h + 1) / G;
-        const double* g = xbuf(h);
-        for (long long j = a0 + threadIdx.x; j < a1; j += kThreads) psi_s[j] = g[j];
+      for (long long j = threadIdx.x; j < n; j += kThreads) {  // owner of column j
+        int h = (int)((j * G) / n);
+        while (h + 1 < G && n * (h + 1) / G <= j) ++h;
+        while (h > 0 && n * h / G > j) --h;
+        psi_s[j] = xbuf(h)[j];
       }
     } else {
       for (long long j = threadIdx.x; j < n; j += kThreads) psi_s[j] = __ldcg(psi + j);
