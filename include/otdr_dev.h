@@ -83,7 +83,8 @@ typedef struct {
    * residual scalars are ncclAllReduce'd once per iteration. */
   int rank, nranks;
   int64_t row_begin, row_end;
-  const unsigned char* nccl_id; /* 128-byte ncclUniqueId when nranks > 1 */
+  const unsigned char* nccl_id; /* 128-byte ncclUniqueId; required when nranks > 1, optional
+                                  for nranks == 1 (runs the NCCL exchange path on one GPU) */
 } otdr_dev_config;
 
 typedef struct {

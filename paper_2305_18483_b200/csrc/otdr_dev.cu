@@ -120,6 +120,7 @@ struct otdr_dev {
   bool use_fused_finalize = false;
   // on-chip resident solve (plans that fit the GPU's aggregate shared memory)
   bool allow_resident = true;
+  bool sharded = false;  // NCCL exchange path (row shards, or a 1-rank communicator)
   int res_G = 0, res_R = 0;
   size_t res_smem = 0;
   double* gscratch = nullptr;
@@ -410,7 +411,7 @@ struct otdr_dev {
     res_G = 0;
     res_R = 0;
     res_smem = 0;
-    if (!allow_resident || comm || m_loc < 1 || reg_kind == OTDR_REG_GROUP_LASSO) return;
+    if (!allow_resident || sharded || m_loc < 1 || reg_kind == OTDR_REG_GROUP_LASSO) return;
     int max_smem = 0;
     CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg.device));
     const long long G = std::min<long long>(num_sms, m_loc);
@@ -828,8 +829,9 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     // psi padding: -inf keeps padded columns exactly 0 through the clamp.
     std::vector<double> pad(size_t(ctx->ld), -std::numeric_limits<double>::infinity());
     CK(cudaMemcpy(ctx->psi, pad.data(), size_t(ctx->ld) * 8, cudaMemcpyHostToDevice));
+    ctx->sharded = nranks > 1 || cfg->nccl_id != nullptr;
     ctx->build_segments();
-    if (nranks > 1) {
+    if (ctx->sharded) {  // a 1-rank communicator exercises the multi-GPU path on one GPU
       ncclUniqueId id;
       std::memcpy(&id, cfg->nccl_id, sizeof(id));
       NK(nccl().CommInitRank(&ctx->comm, nranks, id, cfg->rank));

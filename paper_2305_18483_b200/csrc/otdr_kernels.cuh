@@ -133,6 +133,36 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return t;
 }
 
+// Reduce-scatter of 8 row partials across a warp: lane l ends with the full
+// sum of row row8_of(l) (lanes with equal bits 2..4 share a row). 9 double
+// shuffles per 8 rows instead of 5 per row; the summation tree is fixed.
+__device__ __forceinline__ int row8_of(int lane) {
+  return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+}
+__device__ __forceinline__ double reduce8_rows(const double (&rs)[8], int lane) {
+  double a4[4];
+  const bool hi16 = (lane & 16) != 0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const double keep = hi16 ? rs[4 + t] : rs[t];
+    const double send = hi16 ? rs[t] : rs[4 + t];
+    a4[t] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  double a2[2];
+  const bool hi8 = (lane & 8) != 0;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const double keep = hi8 ? a4[2 + t] : a4[t];
+    const double send = hi8 ? a4[t] : a4[2 + t];
+    a2[t] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  const bool hi4 = (lane & 4) != 0;
+  double a1 = (hi4 ? a2[1] : a2[0]) + __shfl_xor_sync(0xffffffffu, hi4 ? a2[0] : a2[1], 4);
+  a1 += __shfl_xor_sync(0xffffffffu, a1, 2);
+  a1 += __shfl_xor_sync(0xffffffffu, a1, 1);
+  return a1;
+}
+
 // ---------------------------------------------------------------- sweep
 // Row-major C, X with leading dimension ld (multiple of the vector width;
 // padded columns hold X = 0 and psi = -inf so they stay exactly 0).
@@ -636,38 +666,44 @@ __global__ void __launch_bounds__(NT) gl_cluster_kernel(GLArgs<T> a,
 #pragma unroll
   for (int e = 0; e < VW; ++e) sc[e] = sig[lane * VW + e];
 
-  // phase 2: X = v * scale, row partials, column partials
-  for (int t = warp; t < nrows; t += NW) {
-    const long long i = r0 + t;
-    double rs = 0.0;
-    if (cok) {
-      const T* vr = tileX + (size_t)t * TN + lane * VW;
-      double v[VW], o[VW];
-      if constexpr (VW * sizeof(T) == 16) {
-        unpack(*reinterpret_cast<const typename Vec<T>::type*>(vr), v);
-      } else {
+  // phase 2: X = v * scale, row partials (8-row reduce-scatter), column partials
+  for (int t0 = warp * 8; t0 < nrows; t0 += NW * 8) {
+    double rs[8];
 #pragma unroll
-        for (int e = 0; e < VW; ++e) v[e] = (double)vr[e];
-      }
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u;
+      rs[u] = 0.0;
+      if (cok && t < nrows) {
+        const long long i = r0 + t;
+        const T* vr = tileX + (size_t)t * TN + lane * VW;
+        double v[VW], o[VW];
+        if constexpr (VW * sizeof(T) == 16) {
+          unpack(*reinterpret_cast<const typename Vec<T>::type*>(vr), v);
+        } else {
 #pragma unroll
-      for (int e = 0; e < VW; ++e) {
-        const double nx = sg.grouped ? (EXACT ? __dmul_rn(v[e], sc[e]) : v[e] * sc[e]) : v[e];
-        o[e] = nx;
-        cacc[e] += nx;
-        rs += nx;
-      }
-      if constexpr (VW * sizeof(T) == 16) {
-        *reinterpret_cast<typename Vec<T>::type*>(a.X + i * a.ld + col0) = pack<T>(o);
-      } else if constexpr (VW == 2 && sizeof(T) == 4) {
-        *reinterpret_cast<float2*>(a.X + i * a.ld + col0) =
-            make_float2(__double2float_rn(o[0]), __double2float_rn(o[1]));
-      } else {
+          for (int e = 0; e < VW; ++e) v[e] = (double)vr[e];
+        }
 #pragma unroll
-        for (int e = 0; e < VW; ++e) a.X[i * a.ld + col0 + e] = (T)o[e];
+        for (int e = 0; e < VW; ++e) {
+          const double nx = sg.grouped ? (EXACT ? __dmul_rn(v[e], sc[e]) : v[e] * sc[e]) : v[e];
+          o[e] = nx;
+          cacc[e] += nx;
+          rs[u] += nx;
+        }
+        if constexpr (VW * sizeof(T) == 16) {
+          *reinterpret_cast<typename Vec<T>::type*>(a.X + i * a.ld + col0) = pack<T>(o);
+        } else if constexpr (VW == 2 && sizeof(T) == 4) {
+          *reinterpret_cast<float2*>(a.X + i * a.ld + col0) =
+              make_float2(__double2float_rn(o[0]), __double2float_rn(o[1]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < VW; ++e) a.X[i * a.ld + col0 + e] = (T)o[e];
+        }
       }
     }
-    rs = warp_sum(rs);
-    if (lane == 0) a.rowpart[i * (long long)nstripes + stripe] = rs;
+    const double tot = reduce8_rows(rs, lane);
+    const int t = t0 + row8_of(lane);
+    if ((lane & 3) == 0 && t < nrows) a.rowpart[(r0 + t) * (long long)nstripes + stripe] = tot;
   }
   __syncthreads();
 #pragma unroll

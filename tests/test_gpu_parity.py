@@ -484,3 +484,29 @@ def test_batched_device_cost_and_512(ora):
         assert reps[b].termination.name == "Converged"
         assert abs(reps[b].iterations - o.iterations) <= 3
         assert abs(reps[b].objective - o.objective) <= 1e-6 * abs(o.objective)
+
+
+@pytest.mark.parametrize("kind", ["quad", "gl"])
+def test_nccl_exchange_path_single_rank(ora, kind):
+    """The row-sharded code path (reduce -> ncclAllReduce -> update, chunked
+    host-polled graphs) on a 1-rank NCCL communicator equals the single-GPU path."""
+    from paper_2305_18483_b200 import sharding
+    m, n = 300, 257
+    C, p, q, src, tgt, ls, lt = ora.adaptation_problem(m, n, 3, 1)
+    reg = otdr.QuadraticReg(2.0) if kind == "quad" else otdr.GroupLassoReg(2e-3, otdr.column_class_blocks(ls, n))
+    outs = []
+    for shard in (None, otdr.Shard(0, 1, 0, m, sharding.nccl_unique_id())):
+        eng = otdr.Engine(m, n, "f64", shard=shard)
+        eng.set_problem(C, p, q)
+        eng.set_regularizer(reg)
+        eng.set_state()
+        eng.step(otdr.default_stepsize(m, n), 25)
+        st = eng.get_state()
+        eng.set_state()
+        rep = eng.solve(otdr.SolverOptions(tol_primal=1e-6, max_iter=5000))
+        outs.append((st, rep))
+        eng.close()
+    (a, ra), (b, rb) = outs
+    assert rel(a.X, b.X) <= 1e-12 and rel(a.phi, b.phi) <= 1e-12 and rel(a.psi, b.psi) <= 1e-12
+    assert ra.termination == rb.termination and abs(ra.iterations - rb.iterations) <= 1
+    assert abs(ra.objective - rb.objective) <= 1e-10 * abs(ra.objective)
