@@ -22,6 +22,8 @@
  *   otdr_dev_objective              primal_objective             problem.hpp:32-33
  *   otdr_dev_duality_gap            duality_gap                  duality.hpp:31-32
  *   otdr_dev_get_trace              SolveReport::trace           solver.hpp:65-72
+ *   otdr_dev_read_cost_otpb /       read_matrix_otpb /           io.cpp:127-158
+ *   otdr_dev_write_plan_otpb        write_matrix_otpb (plan)
  *   otdr_dev_last_error             exception what() text        errors.hpp:9-34
  *
  * Errors: every call returns an otdr_status; the matching exception text of the
@@ -159,6 +161,17 @@ otdr_status otdr_dev_load_state(otdr_dev* ctx, const double* X, const double* ph
                                 const double* psi, const double* a, const double* b,
                                 const double* r, const double* s, double theta, double eta,
                                 int64_t k);
+/* OTPB plan I/O straight from / to device buffers (io.cpp:127-158 format:
+ * 16-byte header "OTPB", u32 m, u32 n, 4 zero bytes, then m*n fp64
+ * row-major). read: the local rows of an m x n cost file become C (values
+ * checked finite and >= 0 -> OTDR_E_NEGATIVE, shape -> OTDR_E_DIMENSION,
+ * bad magic / truncation -> OTDR_E_INVALID_ARG); p, q as in set_problem.
+ * write: the local rows of the current plan X land at their global offset,
+ * so the ranks of a row-sharded run write one file together (the rank owning
+ * row 0 writes the header). */
+otdr_status otdr_dev_read_cost_otpb(otdr_dev* ctx, const char* path, const double* p,
+                                    const double* q);
+otdr_status otdr_dev_write_plan_otpb(otdr_dev* ctx, const char* path);
 /* iters raw DR steps (no stopping logic), like calling step() iters times. */
 otdr_status otdr_dev_step(otdr_dev* ctx, double rho, int64_t iters);
 /* Runs the solve loop from the current state with the reference's stopping

@@ -66,7 +66,7 @@ EXPORTS = [
     "otdr_dev_set_regularizer", "otdr_dev_set_state", "otdr_dev_load_state", "otdr_dev_step",
     "otdr_dev_solve", "otdr_dev_get_state", "otdr_dev_objective", "otdr_dev_duality_gap",
     "otdr_dev_get_trace", "otdr_dev_profile", "otdr_dev_time_steps",
-    "otdr_dev_kernels_per_iteration",
+    "otdr_dev_kernels_per_iteration", "otdr_dev_read_cost_otpb", "otdr_dev_write_plan_otpb",
     "otdr_batch_create", "otdr_batch_destroy", "otdr_batch_last_error", "otdr_batch_set_problems",
     "otdr_batch_build_sqdist_costs", "otdr_batch_set_regularizer", "otdr_batch_solve",
     "otdr_batch_get_plans",
@@ -109,6 +109,8 @@ def lib():
     L.otdr_dev_get_trace.argtypes = [vp, ct.POINTER(TraceRow), ct.c_int64, _i64p]
     L.otdr_dev_profile.argtypes = [vp, ct.c_double, ct.c_int64, ct.POINTER(KernelTimes)]
     L.otdr_dev_time_steps.argtypes = [vp, ct.c_double, ct.c_int64, _dp]
+    L.otdr_dev_read_cost_otpb.argtypes = [vp, ct.c_char_p, _dp, _dp]
+    L.otdr_dev_write_plan_otpb.argtypes = [vp, ct.c_char_p]
     L.otdr_gaussian_points.argtypes = [ct.c_int64, ct.c_int64, ct.c_uint64, _dp, _dp]
     L.otdr_gaussian_points.restype = None
     L.otdr_adaptation_points.argtypes = [ct.c_int64, ct.c_int64, ct.c_int, ct.c_uint64, ct.c_int,

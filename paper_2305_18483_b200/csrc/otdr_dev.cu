@@ -14,6 +14,8 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <unistd.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -912,6 +914,134 @@ otdr_status otdr_dev_build_sqdist_cost(otdr_dev* ctx, const double* src_pts,
     CK(cudaMemcpy(ctx->q, q, size_t(ctx->n) * 8, cudaMemcpyHostToDevice));
     ctx->has_problem = true;
     ctx->has_state = false;
+    return OTDR_OK;
+  });
+}
+
+namespace {
+
+struct Fd {  // RAII file descriptor
+  int fd = -1;
+  ~Fd() {
+    if (fd >= 0) ::close(fd);
+  }
+};
+
+bool pread_all(int fd, void* buf, size_t bytes, off_t off) {
+  char* p = static_cast<char*>(buf);
+  while (bytes > 0) {
+    const ssize_t r = ::pread(fd, p, bytes, off);
+    if (r <= 0) return false;
+    p += r;
+    off += r;
+    bytes -= size_t(r);
+  }
+  return true;
+}
+
+bool pwrite_all(int fd, const void* buf, size_t bytes, off_t off) {
+  const char* p = static_cast<const char*>(buf);
+  while (bytes > 0) {
+    const ssize_t r = ::pwrite(fd, p, bytes, off);
+    if (r <= 0) return false;
+    p += r;
+    off += r;
+    bytes -= size_t(r);
+  }
+  return true;
+}
+
+}  // namespace
+
+otdr_status otdr_dev_read_cost_otpb(otdr_dev* ctx, const char* path, const double* p,
+                                    const double* q) {
+  if (!ctx) return OTDR_E_INVALID_ARG;
+  if (!path || !p || !q) return fail(ctx, OTDR_E_INVALID_ARG, "null argument");
+  return guarded(ctx, [&] {
+    Fd f;
+    f.fd = ::open(path, O_RDONLY);
+    if (f.fd < 0) return fail(ctx, OTDR_E_INVALID_ARG, std::string(path) + ": cannot open");
+    unsigned char hdr[16];
+    if (!pread_all(f.fd, hdr, 16, 0) || std::memcmp(hdr, "OTPB", 4) != 0)
+      return fail(ctx, OTDR_E_INVALID_ARG, std::string(path) + ": not an OTPB file (bad magic)");
+    uint32_t m32 = 0, n32 = 0;
+    std::memcpy(&m32, hdr + 4, 4);
+    std::memcpy(&n32, hdr + 8, 4);
+    if ((long long)m32 != ctx->m_glob || (long long)n32 != ctx->n)
+      return fail(ctx, OTDR_E_DIMENSION,
+                  std::string(path) + ": OTPB is " + std::to_string(m32) + "x" +
+                      std::to_string(n32) + ", context is " + std::to_string(ctx->m_glob) + "x" +
+                      std::to_string(ctx->n));
+    const long long n = ctx->n;
+    const long long rows_per = std::max<long long>(1, (long long)(kStageDoubles / size_t(n)));
+    std::vector<double> host;
+    for (long long r0 = 0; r0 < ctx->m_loc; r0 += rows_per) {
+      const long long rows = std::min(rows_per, ctx->m_loc - r0);
+      host.resize(size_t(rows * n));
+      const off_t off = 16 + off_t((ctx->row0 + r0) * n) * 8;
+      if (!pread_all(f.fd, host.data(), host.size() * 8, off))
+        return fail(ctx, OTDR_E_INVALID_ARG, std::string(path) + ": truncated OTPB payload");
+      for (size_t t = 0; t < host.size(); ++t)
+        if (!(host[t] >= 0.0) || !std::isfinite(host[t]))
+          return fail(ctx, OTDR_E_NEGATIVE,
+                      "cost(" + std::to_string(ctx->row0 + r0 + (long long)t / n) + "," +
+                          std::to_string((long long)t % n) + ") must be finite and >= 0");
+      CK(cudaMemcpy(ctx->stage, host.data(), host.size() * 8, cudaMemcpyHostToDevice));
+      if (ctx->f64())
+        otdrk::scatter_rows_kernel<double><<<4 * kNumSMs, 256, 0, ctx->stream>>>(
+            (double*)ctx->C, ctx->stage, ctx->d_dev_row + r0, rows, n, ctx->ld);
+      else
+        otdrk::scatter_rows_kernel<float><<<4 * kNumSMs, 256, 0, ctx->stream>>>(
+            (float*)ctx->C, ctx->stage, ctx->d_dev_row + r0, rows, n, ctx->ld);
+      ctx->check_launch();
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
+    ctx->h_p.assign(p, p + ctx->m_loc);
+    ctx->h_q.assign(q, q + ctx->n);
+    ctx->upload_vec_rows(ctx->p, p);
+    CK(cudaMemcpy(ctx->q, q, size_t(ctx->n) * 8, cudaMemcpyHostToDevice));
+    ctx->has_problem = true;
+    ctx->has_state = false;
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_write_plan_otpb(otdr_dev* ctx, const char* path) {
+  if (!ctx || !path) return OTDR_E_INVALID_ARG;
+  if (!ctx->has_state) return fail(ctx, OTDR_E_STATE, "write_plan before set_state");
+  return guarded(ctx, [&] {
+    Fd f;
+    const int flags = O_WRONLY | O_CREAT | (ctx->sharded ? 0 : O_TRUNC);
+    f.fd = ::open(path, flags, 0644);
+    if (f.fd < 0) return fail(ctx, OTDR_E_INVALID_ARG, std::string(path) + ": cannot open for writing");
+    if (ctx->row0 == 0) {
+      unsigned char hdr[16] = {'O', 'T', 'P', 'B'};
+      const uint32_t m32 = uint32_t(ctx->m_glob), n32 = uint32_t(ctx->n);
+      std::memcpy(hdr + 4, &m32, 4);
+      std::memcpy(hdr + 8, &n32, 4);
+      if (!pwrite_all(f.fd, hdr, 16, 0))
+        return fail(ctx, OTDR_E_INVALID_ARG, std::string(path) + ": write failed");
+    }
+    const long long n = ctx->n;
+    const long long rows_per = std::max<long long>(1, (long long)(kStageDoubles / size_t(n)));
+    std::vector<double> host;
+    for (long long r0 = 0; r0 < ctx->m_loc; r0 += rows_per) {
+      const long long rows = std::min(rows_per, ctx->m_loc - r0);
+      if (ctx->f64())
+        otdrk::gather_rows_kernel<double><<<4 * kNumSMs, 256, 0, ctx->stream>>>(
+            ctx->stage, (const double*)ctx->X, ctx->d_dev_row + r0, rows, n, ctx->ld);
+      else
+        otdrk::gather_rows_kernel<float><<<4 * kNumSMs, 256, 0, ctx->stream>>>(
+            ctx->stage, (const float*)ctx->X, ctx->d_dev_row + r0, rows, n, ctx->ld);
+      ctx->check_launch();
+      host.resize(size_t(rows * n));
+      CK(cudaMemcpyAsync(host.data(), ctx->stage, host.size() * 8, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      const off_t off = 16 + off_t((ctx->row0 + r0) * n) * 8;
+      if (!pwrite_all(f.fd, host.data(), host.size() * 8, off))
+        return fail(ctx, OTDR_E_INVALID_ARG, std::string(path) + ": write failed");
+    }
     return OTDR_OK;
   });
 }

@@ -462,6 +462,16 @@ class Engine:
         q = _f64(q, (self.n,))
         self._ck(self._L.otdr_dev_set_problem(self._h, nat.dptr(C), nat.dptr(p), nat.dptr(q)))
 
+    def read_cost_otpb(self, path: str, p_local, q):
+        """Load this engine's rows of an OTPB cost file (io.cpp:127-158) into HBM."""
+        p = _f64(p_local, (self.m_local,))
+        q = _f64(q, (self.n,))
+        self._ck(self._L.otdr_dev_read_cost_otpb(self._h, str(path).encode(), nat.dptr(p), nat.dptr(q)))
+
+    def write_plan_otpb(self, path: str):
+        """Write the plan (this engine's rows) as OTPB straight from HBM."""
+        self._ck(self._L.otdr_dev_write_plan_otpb(self._h, str(path).encode()))
+
     def build_sqdist_cost(self, src_local, tgt, p_local, q) -> bool:
         src = _f64(src_local)
         tgt = _f64(tgt)

@@ -102,3 +102,17 @@ def test_skip_count_and_init_mirror_oracle(ora):
         otdr.QuadraticReg(0.0)
     with pytest.raises(otdr.InvalidArgument):
         otdr.GroupLassoReg(-1.0, otdr.column_class_blocks([0], 1))
+
+
+def test_otpb_host_roundtrip(tmp_path):
+    from paper_2305_18483_b200 import io
+    a = np.arange(12, dtype=np.float64).reshape(3, 4) / 7.0
+    path = str(tmp_path / "a.otpb")
+    io.write_matrix_otpb(path, a)
+    raw = open(path, "rb").read()
+    assert raw[:4] == b"OTPB" and raw[4:8] == (3).to_bytes(4, "little") and raw[12:16] == b"\0" * 4
+    assert len(raw) == 16 + 12 * 8
+    assert np.array_equal(io.read_matrix_otpb(path), a)
+    open(path, "r+b").write(b"XXXX")
+    with pytest.raises(otdr.InvalidArgument):
+        io.read_matrix_otpb(path)

@@ -510,3 +510,37 @@ def test_nccl_exchange_path_single_rank(ora, kind):
     assert rel(a.X, b.X) <= 1e-12 and rel(a.phi, b.phi) <= 1e-12 and rel(a.psi, b.psi) <= 1e-12
     assert ra.termination == rb.termination and abs(ra.iterations - rb.iterations) <= 1
     assert abs(ra.objective - rb.objective) <= 1e-10 * abs(ra.objective)
+
+
+@pytest.mark.parametrize("storage", ["f64", "f32"])
+def test_otpb_device_io(ora, tmp_path, storage):
+    """Cost read from an OTPB file straight into HBM, plan written back."""
+    from paper_2305_18483_b200 import io
+    m, n = 157, 211
+    C, p, q, *_ = ora.gaussian_problem(m, n, 4)
+    cpath, xpath = str(tmp_path / "c.otpb"), str(tmp_path / "x.otpb")
+    io.write_matrix_otpb(cpath, C)
+    eng = otdr.Engine(m, n, storage)
+    eng.read_cost_otpb(cpath, p, q)
+    eng.set_regularizer(otdr.QuadraticReg(1.5))
+    eng.set_state()
+    eng.step(otdr.default_stepsize(m, n), 30)
+    eng.write_plan_otpb(xpath)
+    st = eng.get_state()
+    assert np.array_equal(io.read_matrix_otpb(xpath), st.X)
+    ref = otdr.Engine(m, n, storage)
+    ref.set_problem(C, p, q)
+    ref.set_regularizer(otdr.QuadraticReg(1.5))
+    ref.set_state()
+    ref.step(otdr.default_stepsize(m, n), 30)
+    assert np.array_equal(ref.get_state().X, st.X)
+    io.write_matrix_otpb(cpath, C[:, :-1])
+    with pytest.raises(otdr.DimensionMismatch):
+        eng.read_cost_otpb(cpath, p, q)
+    bad = C.copy()
+    bad[3, 4] = -1.0
+    io.write_matrix_otpb(cpath, bad)
+    with pytest.raises(otdr.NegativeEntry):
+        eng.read_cost_otpb(cpath, p, q)
+    eng.close()
+    ref.close()
