@@ -82,7 +82,7 @@ struct otdr_batch {
                            reg == OTDR_REG_QUAD ? otdrk::REG_QUAD : otdrk::REG_NONE, 0};
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(unsigned(B * G), 1, 1);
-    lc.blockDim = dim3(otdrk::kThreads, 1, 1);
+    lc.blockDim = dim3(otdrk::kRT, 1, 1);
     lc.dynamicSmemBytes = smem;
     lc.stream = stream;
     cudaLaunchAttribute attr[1];

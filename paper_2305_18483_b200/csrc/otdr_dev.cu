@@ -437,7 +437,7 @@ struct otdr_dev {
                            reg_kind == OTDR_REG_QUAD ? otdrk::REG_QUAD : otdrk::REG_NONE, iters};
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(unsigned(res_G), 1, 1);
-    lc.blockDim = dim3(otdrk::kThreads, 1, 1);
+    lc.blockDim = dim3(otdrk::kRT, 1, 1);
     lc.dynamicSmemBytes = res_smem;
     lc.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -493,7 +493,7 @@ struct otdr_dev {
       glc_rows = int(rows);
       const size_t creg = std::max(size_t(rows) * size_t(row_bytes),
                                    size_t(kGLThreads / 32) * size_t(tn) * 8);
-      glc_smem = size_t(rows) * size_t(row_bytes) + creg + 2 * size_t(tn) * 8 +
+      glc_smem = size_t(rows) * size_t(row_bytes) + creg + size_t(k + 1) * size_t(tn) * 8 +
                  size_t(rows) * 8 + 16;
       gl_stripes = int((ld + tn - 1) / tn);
       encode_map(&glc_mapX, X, tn, glc_rows);

@@ -563,8 +563,8 @@ __global__ void __launch_bounds__(NT) gl_cluster_kernel(GLArgs<T> a,
   T* tileC = tileX + (size_t)R * TN;                          // R x TN (then reduction scratch)
   double* red = reinterpret_cast<double*>(tileC);             // NW x TN, after phase 1
   const size_t creg = max((size_t)R * TN * sizeof(T), (size_t)NW * TN * sizeof(double));
-  double* psq = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(tileC) + creg);  // TN
-  double* sig = psq + TN;                                     // TN
+  double* psq = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(tileC) + creg);  // K x TN
+  double* sig = psq + (size_t)K * TN;                         // TN
   double* phs = sig + TN;                                     // R (phi of own rows)
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(phs + R);
 
@@ -593,6 +593,9 @@ __global__ void __launch_bounds__(NT) gl_cluster_kernel(GLArgs<T> a,
     }
   }
   for (int t = threadIdx.x; t < nrows; t += NT) phs[t] = a.phi[r0 + t];
+  // split cluster barrier: arrive now, wait before the first DSMEM store, so
+  // every peer CTA has started before its shared memory is written
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   double psi_r[VW], sq[VW], cacc[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
@@ -642,26 +645,31 @@ __global__ void __launch_bounds__(NT) gl_cluster_kernel(GLArgs<T> a,
     for (int e = 0; e < VW; ++e) red[warp * TN + lane * VW + e] = sq[e];
   }
   __syncthreads();
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   if (sg.grouped) {
-    for (int t = threadIdx.x; t < TN; t += NT) {
+    // push this CTA's per-column partial norms into slot [crank] of every
+    // peer's table (DSMEM stores), so that after ONE cluster barrier each CTA
+    // reads only its own shared memory
+    for (int t = threadIdx.x; t < TN * K; t += NT) {
+      const int col = t % TN, k = t / TN;
       double s = 0.0;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) s += red[w * TN + t];
-      psq[t] = s;
+      for (int w = 0; w < NW; ++w) s += red[w * TN + col];
+      *cluster.map_shared_rank(psq + (size_t)crank * TN + col, k) = s;
     }
   }
-  cluster.sync();  // partial norms of every CTA visible cluster-wide
+  cluster.sync();  // every CTA's partial norms are in every CTA's table
   if (sg.grouped) {
     for (int t = threadIdx.x; t < TN; t += NT) {
       double s = 0.0;
-      for (int k = 0; k < K; ++k) s += *cluster.map_shared_rank(psq + t, k);  // fixed rank order
+      for (int k = 0; k < K; ++k) s += psq[(size_t)k * TN + t];  // fixed rank order
       const double nrm = sqrt(s);
       sig[t] = (nrm <= thr) ? 0.0 : (EXACT ? __dsub_rn(1.0, __ddiv_rn(thr, nrm)) : 1.0 - thr / nrm);
     }
   } else {
     for (int t = threadIdx.x; t < TN; t += NT) sig[t] = 1.0;
   }
-  cluster.sync();  // remote reads done (psq may be retired) and the scale visible
+  __syncthreads();  // the scale is visible (no DSMEM traffic after the barrier)
   double sc[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) sc[e] = sig[lane * VW + e];

@@ -21,6 +21,22 @@
 
 namespace otdrk {
 
+constexpr int kRT = 512;       // threads per resident CTA
+constexpr int kRW = kRT / 32;  // warps per resident CTA
+
+// Fixed-order block sum over kRW warps (result valid in thread 0).
+__device__ __forceinline__ double block_sum_r(double v, double* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kRW; ++i) t += red[i];
+  return t;
+}
+
 struct ResidentArgs {
   void* X;             // problem b at X + b * mat_stride (elements)
   const void* C;
@@ -50,18 +66,18 @@ struct ResidentArgs {
 template <typename T>
 __host__ __device__ inline int resident_row_sets(long long ld) {
   const long long nch = (ld + 32 * Vec<T>::N - 1) / (32 * Vec<T>::N);
-  return nch >= kWarps ? 1 : (int)(kWarps / nch);
+  return nch >= kRW ? 1 : (int)(kRW / nch);
 }
 
 template <typename T>
 __host__ __device__ inline size_t resident_smem_bytes(long long R, long long n, long long ld) {
   const int sets = resident_row_sets<T>(ld);
   return size_t(2 * R * ld) * sizeof(T) + size_t(n + 4) * 8 + size_t(n) * 8 +
-         size_t(R) * kWarps * 8 + size_t(R) * 16 + (sets > 1 ? size_t(sets) * ld * 8 : 0) + 64;
+         size_t(R) * kRW * 8 + size_t(R) * 16 + (sets > 1 ? size_t(sets) * ld * 8 : 0) + 64;
 }
 
 template <typename T, bool CLUSTER>
-__global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
+__global__ void __launch_bounds__(kRT, 1) resident_kernel(ResidentArgs A) {
   namespace cg = cooperative_groups;
   using V = typename Vec<T>::type;
   constexpr int VEC = Vec<T>::N;
@@ -96,12 +112,12 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
   double* xrow = reinterpret_cast<double*>(Xt + (size_t)R * ld);  // n + 4
   double* psi_s = xrow + n + 4;                                     // n
   double* rowp = psi_s + n;                                         // R * kWarps
-  double* phi_s = rowp + (size_t)R * kWarps;                        // R
+  double* phi_s = rowp + (size_t)R * kRW;                           // R
   double* r_s = phi_s + R;                                          // R
   double* colbuf = r_s + R;                                         // sets x ld (sets > 1)
   const int nsets = resident_row_sets<T>(ld);
   const long long nch = (ld + 32 * VEC - 1) / (32 * VEC);
-  __shared__ double red[kWarps];
+  __shared__ double red[kRW];
   __shared__ double bc[4];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -149,12 +165,12 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
     const V* xs = reinterpret_cast<const V*>(Xg + i0 * ld);
     V* cd = reinterpret_cast<V*>(Ct);
     V* xd = reinterpret_cast<V*>(Xt);
-    for (long long t = threadIdx.x; t < elems / VEC; t += kThreads) {
+    for (long long t = threadIdx.x; t < elems / VEC; t += kRT) {
       cd[t] = cs[t];
       xd[t] = xs[t];
     }
-    for (long long j = threadIdx.x; j < n; j += kThreads) psi_s[j] = psi[j];
-    for (int t = threadIdx.x; t < nr; t += kThreads) phi_s[t] = phi[i0 + t];
+    for (long long j = threadIdx.x; j < n; j += kRT) psi_s[j] = psi[j];
+    for (int t = threadIdx.x; t < nr; t += kRT) phi_s[t] = phi[i0 + t];
   }
   __syncthreads();
 
@@ -169,13 +185,14 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
   long long it = 0;
 
   for (;;) {
-    // ---- 1. sweep own rows (thread: VEC consecutive columns; warp: 32*VEC)
-    for (int t = threadIdx.x; t < nr * kWarps; t += kThreads) rowp[t] = 0.0;
+    // ---- 1. sweep own rows. Warp w: column chunk(s) of 32*VEC columns and the
+    // 8-row groups g = wset, wset + nsets, ...; row sums by 8-row reduce-scatter.
+    for (int t = threadIdx.x; t < nr * kRW; t += kRT) rowp[t] = 0.0;
     __syncthreads();
-    // Warp w: column chunks c = w % nch (+kWarps...) and rows set, set+nsets, ...
     const int wset = (nsets > 1) ? warp / (int)nch : 0;
     const bool wactive = (nsets > 1) ? (warp < (int)nch * nsets) : true;
-    for (long long c = (nsets > 1) ? warp % nch : warp; wactive && c < nch; c += (nsets > 1) ? nch : kWarps) {
+    for (long long c = (nsets > 1) ? warp % nch : warp; wactive && c < nch;
+         c += (nsets > 1) ? nch : kRW) {
       const long long cb = c * 32 * VEC + (long long)lane * VEC;
       const bool ok = cb < ld;
       double ps[VEC], cacc[VEC];
@@ -184,19 +201,20 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
         ps[e] = (cb + e < n) ? psi_s[cb + e] : -INFINITY;
         cacc[e] = 0.0;
       }
-      // two rows per step: independent shuffle chains overlap
-      for (int t = wset; t < nr; t += 2 * nsets) {
-        const int t2 = t + nsets;
-        const bool has2 = t2 < nr;
-        double rs[2] = {0.0, 0.0};
+      const V* xcol = reinterpret_cast<const V*>(Xt + cb);
+      const V* ccol = reinterpret_cast<const V*>(Ct + cb);
+      const long long ldv = ld / VEC;
+      for (int t0 = wset * 8; t0 < nr; t0 += nsets * 8) {
+        double rs[8];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int tt = u ? t2 : t;
-          if (ok && (u == 0 || has2)) {
-            const double ph = phi_s[tt];
+        for (int u = 0; u < 8; ++u) {
+          const int t = t0 + u;
+          rs[u] = 0.0;
+          if (ok && t < nr) {
+            const double ph = phi_s[t];
             double x[VEC], cc[VEC], o[VEC];
-            unpack(reinterpret_cast<const V*>(Xt + (size_t)tt * ld)[cb / VEC], x);
-            unpack(reinterpret_cast<const V*>(Ct + (size_t)tt * ld)[cb / VEC], cc);
+            unpack(xcol[t * ldv], x);
+            unpack(ccol[t * ldv], cc);
 #pragma unroll
             for (int e = 0; e < VEC; ++e) {
               const double val = exact ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, cc[e])), ph), ps[e])
@@ -207,18 +225,12 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
               cacc[e] += nx;
               rs[u] += nx;
             }
-            reinterpret_cast<V*>(Xt + (size_t)tt * ld)[cb / VEC] = pack<T>(o);
+            const_cast<V*>(xcol)[t * ldv] = pack<T>(o);
           }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          rs[0] += __shfl_xor_sync(0xffffffffu, rs[0], o);
-          rs[1] += __shfl_xor_sync(0xffffffffu, rs[1], o);
-        }
-        if (lane == 0) {
-          rowp[t * kWarps + warp] += rs[0];
-          if (has2) rowp[t2 * kWarps + warp] += rs[1];
-        }
+        const double tot = reduce8_rows(rs, lane);
+        const int row = t0 + row8_of(lane);
+        if ((lane & 3) == 0 && row < nr) rowp[row * kRW + warp] += tot;
       }
       double* cdst = (nsets > 1) ? colbuf + (size_t)wset * ld : xrow;
 #pragma unroll
@@ -227,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
     }
     if (nsets > 1) {  // fold the row subsets' column partials in a fixed order
       __syncthreads();
-      for (long long j = threadIdx.x; j < n; j += kThreads) {
+      for (long long j = threadIdx.x; j < n; j += kRT) {
         double sacc = 0.0;
         for (int w = 0; w < nsets; ++w) sacc += colbuf[(size_t)w * ld + j];
         xrow[j] = sacc;
@@ -236,10 +248,10 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
     __syncthreads();
     // row sums -> r (own rows), scalar partials
     double sr = 0.0, sr2 = 0.0, sR = 0.0;
-    for (int t = threadIdx.x; t < nr; t += kThreads) {
+    for (int t = threadIdx.x; t < nr; t += kRT) {
       double Rr = 0.0;
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) Rr += rowp[t * kWarps + w];
+      for (int w = 0; w < kRW; ++w) Rr += rowp[t * kRW + w];
       const double ri = Rr - pv[i0 + t];
       r_s[t] = ri;
       sr += ri;
@@ -247,9 +259,9 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
       sR += Rr;
     }
     {
-      const double t1 = block_sum(sr, red);
-      const double t2 = block_sum(sr2, red);
-      const double t3 = block_sum(sR, red);
+      const double t1 = block_sum_r(sr, red);
+      const double t2 = block_sum_r(sr2, red);
+      const double t3 = block_sum_r(sR, red);
       if (threadIdx.x == 0) {
         if constexpr (CLUSTER) {
           xrow[n] = t1;
@@ -264,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
       }
       if constexpr (!CLUSTER) {
         double* g = xbuf(rank);
-        for (long long j = threadIdx.x; j < n; j += kThreads) g[j] = xrow[j];
+        for (long long j = threadIdx.x; j < n; j += kRT) g[j] = xrow[j];
       }
     }
     xsync();  // ---- 2. column partials and scalar partials visible
@@ -277,14 +289,14 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
     const double shift = __dsub_rn(2.0 * eta, theta);
     const double rsq = bc[1];
     // ---- 3. own rows: phi, a; owned columns: s, psi, b
-    for (int t = threadIdx.x; t < nr; t += kThreads) {
+    for (int t = threadIdx.x; t < nr; t += kRT) {
       const double ri = r_s[t], ai = av[i0 + t];
       const double ph = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift), dn);
       phi_s[t] = ph;
       av[i0 + t] = __dsub_rn(ai, ri);
     }
     double ssq = 0.0;  // warp per owned column: lanes fold the G partials
-    for (long long j = j0 + warp; j < j1; j += kWarps) {
+    for (long long j = j0 + warp; j < j1; j += kRW) {
       const double S = warp_fold(j);
       if (lane == 0) {
         const double sj = __dsub_rn(S, qv[j]);
@@ -296,26 +308,26 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
       }
     }
     {
-      const double t4 = block_sum(ssq, red);
+      const double t4 = block_sum_r(ssq, red);
       if constexpr (CLUSTER) xsync();  // peers done reading this CTA's column partials
       if (threadIdx.x == 0) {
         if constexpr (CLUSTER) xrow[n + 3] = t4;
         else xbuf(rank)[n + 3] = t4;
       }
       if constexpr (CLUSTER) {  // publish owned psi slice in smem for peers
-        for (long long j = j0 + threadIdx.x; j < j1; j += kThreads) xrow[j] = psi[j];
+        for (long long j = j0 + threadIdx.x; j < j1; j += kRT) xrow[j] = psi[j];
       }
     }
     xsync();  // ---- 4. psi slices and sum s^2 partials visible
     if constexpr (CLUSTER) {
-      for (long long j = threadIdx.x; j < n; j += kThreads) {  // owner of column j
+      for (long long j = threadIdx.x; j < n; j += kRT) {  // owner of column j
         int h = (int)((j * G) / n);
         while (h + 1 < G && n * (h + 1) / G <= j) ++h;
         while (h > 0 && n * h / G > j) --h;
         psi_s[j] = xbuf(h)[j];
       }
     } else {
-      for (long long j = threadIdx.x; j < n; j += kThreads) psi_s[j] = __ldcg(psi + j);
+      for (long long j = threadIdx.x; j < n; j += kRT) psi_s[j] = __ldcg(psi + j);
     }
     if (warp == 0) {
       const double u4 = warp_fold(n + 3);
@@ -379,13 +391,13 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
   {
     double lin = 0.0, xsq = 0.0;
     const long long elems = (long long)nr * ld;
-    for (long long t = threadIdx.x; t < elems; t += kThreads) {
+    for (long long t = threadIdx.x; t < elems; t += kRT) {
       const double xv = (double)Xt[t], cv = (double)Ct[t];
       lin += cv * xv;
       xsq += xv * xv;
     }
-    const double t1 = block_sum(lin, red);
-    const double t2 = block_sum(xsq, red);
+    const double t1 = block_sum_r(lin, red);
+    const double t2 = block_sum_r(xsq, red);
     if (threadIdx.x == 0) {
       double* g = CLUSTER ? xrow : xbuf(rank);
       g[n] = t1;
@@ -402,8 +414,8 @@ __global__ void __launch_bounds__(kThreads, 1) resident_kernel(ResidentArgs A) {
     const long long elems = (long long)nr * ld;
     V* xd = reinterpret_cast<V*>(Xg + i0 * ld);
     const V* xs = reinterpret_cast<const V*>(Xt);
-    for (long long t = threadIdx.x; t < elems / VEC; t += kThreads) xd[t] = xs[t];
-    for (int t = threadIdx.x; t < nr; t += kThreads) {
+    for (long long t = threadIdx.x; t < elems / VEC; t += kRT) xd[t] = xs[t];
+    for (int t = threadIdx.x; t < nr; t += kRT) {
       phi[i0 + t] = phi_s[t];
       rv[i0 + t] = r_s[t];
     }
