@@ -172,6 +172,8 @@ def main():
             run_batched("cfg5", 256, 512, "f32")
         elif c == "cfg5-seq":
             run_batched_sequential("cfg5", 256, 512, "f32")
+        elif c == "headline":
+            run_plain("headline", 20000, 20000, otdr.QuadraticReg(200.0), "f32", a.iters)
         elif c == "headline-fused":
             run_plain("headline", 20000, 20000, otdr.QuadraticReg(200.0), "f32", a.iters, fused=True)
 

@@ -151,6 +151,12 @@ struct otdr_dev {
   int glc_tn = 0, glc_k = 1, glc_rows = 0;
   size_t glc_smem = 0;
   CUtensorMap glc_mapX{}, glc_mapC{};
+  // TMA-pipelined plain sweep (OTDR_SWEEP=tma): box 256 cols x kSweepTR rows
+  bool use_tma_sweep = false;
+  CUtensorMap sw_mapX{}, sw_mapC{};
+  static constexpr int kSweepTR = 16;
+  static constexpr int kSweepStages = 4;     // fp32: 4 x 32 KB ring
+  static constexpr int kSweepStages64 = 3;   // fp64: 3 x 64 KB ring
   int RB = 1, CB = 1;
   size_t rowpart_cap = 0, colpart_cap = 0, cpart_cap = 0;
   std::vector<Segment> segs, cert_segs;
@@ -241,6 +247,36 @@ struct otdr_dev {
     }
     dim3 grid(stripes, rowgroups);
     const int so = sums_only ? 1 : 0;
+    if (use_tma_sweep && !sums_only && !track && !prm.fused) {
+      const int S = f64() ? kSweepStages64 : kSweepStages;
+      const size_t smem = 2 * size_t(S) * kSweepTR * 256 * esz + 8 * size_t(S);
+      if (f64()) {
+        otdrk::SweepArgs<double> sa{(double*)X, (const double*)C, phi, psi, rowpart, colpart,
+                                    d_prm, d_ctl, m_loc, ld, rows_per_cta, 0};
+        if (reg_kind == OTDR_REG_QUAD) {
+          auto kern = otdrk::sweep_tma_kernel<double, otdrk::REG_QUAD, true, kSweepStages64, kSweepTR>;
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+          kern<<<grid, otdrk::kThreads, smem, stream>>>(sa, sw_mapX, sw_mapC);
+        } else {
+          auto kern = otdrk::sweep_tma_kernel<double, otdrk::REG_NONE, true, kSweepStages64, kSweepTR>;
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+          kern<<<grid, otdrk::kThreads, smem, stream>>>(sa, sw_mapX, sw_mapC);
+        }
+      } else {
+        otdrk::SweepArgs<float> sa{(float*)X, (const float*)C, phi, psi, rowpart, colpart,
+                                   d_prm, d_ctl, m_loc, ld, rows_per_cta, 0};
+        if (reg_kind == OTDR_REG_QUAD) {
+          auto kern = otdrk::sweep_tma_kernel<float, otdrk::REG_QUAD, false, kSweepStages, kSweepTR>;
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+          kern<<<grid, otdrk::kThreads, smem, stream>>>(sa, sw_mapX, sw_mapC);
+        } else {
+          auto kern = otdrk::sweep_tma_kernel<float, otdrk::REG_NONE, false, kSweepStages, kSweepTR>;
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+          kern<<<grid, otdrk::kThreads, smem, stream>>>(sa, sw_mapX, sw_mapC);
+        }
+      }
+      return;
+    }
     if (f64()) {
       otdrk::SweepArgs<double> sa{(double*)X, (const double*)C, phi, psi, rowpart, colpart,
                                   d_prm, d_ctl, m_loc, ld, rows_per_cta, so};
@@ -397,6 +433,10 @@ struct otdr_dev {
     num_cert_segs = int(cert_segs.size());
     plan_gl_cluster();
     plan_resident();
+    if (use_tma_sweep && m_loc > 0) {
+      encode_map(&sw_mapX, X, 256, kSweepTR);
+      encode_map(&sw_mapC, C, 256, kSweepTR);
+    }
     if (d_seg) cudaFree(d_seg);
     if (d_cert_seg) cudaFree(d_cert_seg);
     d_seg = dalloc<Segment>(segs.size());
@@ -797,6 +837,7 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
     if (const char* fe = std::getenv("OTDR_FINALIZE")) ctx->use_fused_finalize = std::strcmp(fe, "fused") == 0;
     if (const char* re = std::getenv("OTDR_RESIDENT")) ctx->allow_resident = std::strcmp(re, "off") != 0;
+    if (const char* se = std::getenv("OTDR_SWEEP")) ctx->use_tma_sweep = std::strcmp(se, "tma") == 0;
     {
       int occ = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, otdrk::finalize_kernel,

@@ -728,6 +728,134 @@ __global__ void __launch_bounds__(NT) gl_cluster_kernel(GLArgs<T> a,
   }
 }
 
+// --------------------------------------------------- TMA-pipelined sweep
+// The plain iteration (zero / quadratic, not fused, untracked) with C and X
+// tiles staged by 2-D TMA through an S-stage shared-memory ring: the CTA keeps
+// S-1 tiles (TR rows x 256 columns of C and X) in flight while it computes
+// the oldest one, so HBM sees a steady stream independent of register
+// pressure. Same partial-sum layout as sweep_kernel (rowpart[row][stripe],
+// colpart[rowgroup][col]) and the same element-wise arithmetic.
+template <typename T, int REG, bool EXACT, int S, int TR>
+__global__ void __launch_bounds__(kThreads, 1) sweep_tma_kernel(SweepArgs<T> a,
+                                                                const __grid_constant__ CUtensorMap mapX,
+                                                                const __grid_constant__ CUtensorMap mapC) {
+  using V = typename Vec<T>::type;
+  constexpr int VEC = Vec<T>::N;
+  constexpr int TN = 256;
+  constexpr int NV = TN / (32 * VEC);
+  constexpr unsigned kTileBytes = (unsigned)(TR * TN * sizeof(T));
+  const Ctl* ctl = a.ctl;
+  if (ctl->done) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* ring = reinterpret_cast<T*>(smem_raw);  // S x {X tile, C tile}
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + 2 * S * kTileBytes);
+  __shared__ double red[kWarps][TN];
+
+  const Params& prm = *a.prm;
+  const double rho = prm.rho, qd = prm.quad_d, qinv = prm.quad_inv;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long stripe = blockIdx.x;
+  const long long col0 = stripe * TN;
+  const long long r_begin = (long long)blockIdx.y * a.rows_per_cta;
+  long long r_end = r_begin + a.rows_per_cta;
+  if (r_end > a.m) r_end = a.m;
+  const int ntiles = r_end > r_begin ? (int)((r_end - r_begin + TR - 1) / TR) : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < S && s < ntiles; ++s) {
+      T* xt = ring + (size_t)s * 2 * TR * TN;
+      mbar_expect_tx(&full[s], 2 * kTileBytes);
+      tma_load_2d(xt, &mapX, (int)col0, (int)(r_begin + (long long)s * TR), &full[s]);
+      tma_load_2d(xt + TR * TN, &mapC, (int)col0, (int)(r_begin + (long long)s * TR), &full[s]);
+    }
+  }
+  long long cols[NV];
+  bool cok[NV];
+  double psi_r[NV][VEC], cacc[NV][VEC];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    cols[v] = col0 + v * 32 * VEC + lane * VEC;
+    cok[v] = cols[v] < a.ld;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      psi_r[v][e] = cok[v] ? a.psi[cols[v] + e] : 0.0;
+      cacc[v][e] = 0.0;
+    }
+  }
+  __syncthreads();
+
+  for (int it = 0; it < ntiles; ++it) {
+    const int s = it % S;
+    mbar_wait(&full[s], (unsigned)((it / S) & 1));
+    const T* xt = ring + (size_t)s * 2 * TR * TN;
+    const T* ct = xt + TR * TN;
+    const long long row0 = r_begin + (long long)it * TR;
+    // TR/kWarps rows per warp, their shuffle chains interleaved
+    constexpr int RPW = TR / kWarps;
+    double rs[RPW];
+#pragma unroll
+    for (int u = 0; u < RPW; ++u) {
+      const int t = warp + u * kWarps;
+      const long long i = row0 + t;
+      rs[u] = 0.0;
+      if (i < r_end) {
+        const double ph = a.phi[i];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          if (!cok[v]) continue;
+          double x[VEC], c[VEC], o[VEC];
+          unpack(reinterpret_cast<const V*>(xt + (size_t)t * TN)[v * 32 + lane], x);
+          unpack(reinterpret_cast<const V*>(ct + (size_t)t * TN)[v * 32 + lane], c);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, c[e])), ph), psi_r[v][e])
+                                     : (fma(-rho, c[e], x[e]) + ph) + psi_r[v][e];
+            double nx = clamp0(val);
+            if (REG == REG_QUAD) nx = EXACT ? __ddiv_rn(nx, qd) : nx * qinv;
+            o[e] = nx;
+            cacc[v][e] += nx;
+            rs[u] += nx;
+          }
+          reinterpret_cast<V*>(a.X + i * a.ld)[cols[v] / VEC] = pack<T>(o);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < RPW; ++u) rs[u] += __shfl_xor_sync(0xffffffffu, rs[u], o);
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < RPW; ++u) {
+        const long long i = row0 + warp + u * kWarps;
+        if (i < r_end) a.rowpart[i * (long long)gridDim.x + stripe] = rs[u];
+      }
+    }
+    __syncthreads();  // stage s fully consumed
+    if (threadIdx.x == 0 && it + S < ntiles) {
+      T* dst = ring + (size_t)s * 2 * TR * TN;
+      mbar_expect_tx(&full[s], 2 * kTileBytes);
+      tma_load_2d(dst, &mapX, (int)col0, (int)(r_begin + (long long)(it + S) * TR), &full[s]);
+      tma_load_2d(dst + TR * TN, &mapC, (int)col0, (int)(r_begin + (long long)(it + S) * TR), &full[s]);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) red[warp][v * 32 * VEC + lane * VEC + e] = cacc[v][e];
+  __syncthreads();
+  for (int t = threadIdx.x; t < TN; t += kThreads) {
+    const long long col = col0 + t;
+    if (col < a.ld) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) s += red[w][t];
+      a.colpart[(long long)blockIdx.y * a.ld + col] = s;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- reduce
 // Blocks [0, RB): rows. R_i = sum_s rowpart[s][i] (stripe order), r_i = R_i - p_i,
 // block partials (sum r, sum r^2, sum R); the last row block folds them in

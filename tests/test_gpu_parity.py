@@ -544,3 +544,24 @@ def test_otpb_device_io(ora, tmp_path, storage):
         eng.read_cost_otpb(cpath, p, q)
     eng.close()
     ref.close()
+
+
+@pytest.mark.parametrize("storage", ["f64", "f32"])
+def test_tma_sweep_matches_register_sweep(ora, monkeypatch, storage):
+    """OTDR_SWEEP=tma (TMA ring) and the register-staged sweep give identical
+    iterates (same element-wise arithmetic and partial layout)."""
+    m, n = 1300, 1111
+    C, p, q, *_ = ora.gaussian_problem(m, n, 6)
+    outs = []
+    for mode in ("tma", "regs"):
+        monkeypatch.setenv("OTDR_SWEEP", mode)
+        monkeypatch.setenv("OTDR_RESIDENT", "off")
+        eng = otdr.Engine(m, n, storage)
+        eng.set_problem(C, p, q)
+        eng.set_regularizer(otdr.QuadraticReg(12.0))
+        eng.set_state()
+        eng.step(otdr.default_stepsize(m, n), 20)
+        outs.append(eng.get_state())
+        eng.close()
+    a, b = outs
+    assert np.array_equal(a.X, b.X) and np.array_equal(a.phi, b.phi) and np.array_equal(a.psi, b.psi)
