@@ -151,6 +151,9 @@ struct otdr_dev {
   int glc_tn = 0, glc_k = 1, glc_rows = 0;
   size_t glc_smem = 0;
   CUtensorMap glc_mapX{}, glc_mapC{};
+  // segment-staged GL sweep: one CTA per (segment, group of glst_g stripes)
+  int glst_g = 0, glst_groups = 0;
+  size_t glst_smem = 0;
   // TMA-pipelined plain sweep (OTDR_SWEEP=tma): box 256 cols x kSweepTR rows
   bool use_tma_sweep = false;
   CUtensorMap sw_mapX{}, sw_mapC{};
@@ -217,9 +220,29 @@ struct otdr_dev {
 
   // The cluster kernel covers the plain (non-fused, untracked) iteration; the
   // even/odd and support-tracking variants use the two-phase kernel.
-  bool gl_cluster_active(bool track) const { return glc_tn > 0 && !track && !prm.fused; }
+  bool gl_stage_active(bool track) const { return glst_g > 0 && !track && !prm.fused; }
+  bool gl_cluster_active(bool track) const {
+    return !gl_stage_active(track) && glc_tn > 0 && !track && !prm.fused;
+  }
 
   void launch_sweep(bool track, bool sums_only) {
+    if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only && gl_stage_active(track)) {
+      const dim3 grid{unsigned(glst_groups), unsigned(num_segs), 1u};
+      if (f64()) {
+        otdrk::GLArgs<double> ga{(double*)X, (const double*)C, phi, psi, rowpart, colpart,
+                                 d_seg, d_prm, d_ctl, m_loc, ld};
+        CK(cudaFuncSetAttribute(otdrk::gl_stage_kernel<double, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(glst_smem)));
+        otdrk::gl_stage_kernel<double, true><<<grid, 512, glst_smem, stream>>>(ga, glst_g);
+      } else {
+        otdrk::GLArgs<float> ga{(float*)X, (const float*)C, phi, psi, rowpart, colpart,
+                                d_seg, d_prm, d_ctl, m_loc, ld};
+        CK(cudaFuncSetAttribute(otdrk::gl_stage_kernel<float, false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(glst_smem)));
+        otdrk::gl_stage_kernel<float, false><<<grid, 512, glst_smem, stream>>>(ga, glst_g);
+      }
+      return;
+    }
     if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only && gl_cluster_active(track)) {
       if (f64()) {
         if (glc_tn == 64) launch_gl_cluster<double, true, 2>();
@@ -306,6 +329,7 @@ struct otdr_dev {
   // by the sweep variant that runs in this configuration.
   std::pair<int, int> partial_shape(bool sums_only, bool track) const {
     if (gl_active(sums_only)) {
+      if (gl_stage_active(track)) return {glst_groups, num_segs};
       if (gl_cluster_active(track)) return {gl_stripes, num_segs * glc_k};
       return {int((ld + tn_seg() - 1) / tn_seg()), num_segs};
     }
@@ -505,10 +529,27 @@ struct otdr_dev {
     glc_rows = 0;
     glc_smem = 0;
     gl_stripes = int((ld + tn_seg() - 1) / tn_seg());
+    glst_g = 0;
+    glst_groups = 0;
+    glst_smem = 0;
     if (reg_kind != OTDR_REG_GROUP_LASSO || m_loc == 0) return;
     long long lmax = 0;
     for (const Segment& sg : segs) lmax = std::max(lmax, sg.end - sg.begin);
     if (lmax == 0) return;
+    // segment-staged kernel: the whole segment's v for a 64-byte stripe in
+    // shared memory (<= 100 KB: two or three CTAs per SM); OTDR_GL_KERNEL
+    // selects stage / cluster / twopass explicitly.
+    const char* gk = std::getenv("OTDR_GL_KERNEL");
+    const bool want_stage = !gk || std::strcmp(gk, "stage") == 0;
+    const size_t stage_bytes = size_t(lmax) * (64 + 8);
+    if (want_stage && stage_bytes <= size_t(100) * 1024) {
+      const long long tn = 64 / (long long)esz;
+      const long long nstr = (ld + tn - 1) / tn;
+      glst_g = 4;  // stripes per CTA: row partials per (row, 4 stripes)
+      glst_groups = int((nstr + glst_g - 1) / glst_g);
+      glst_smem = stage_bytes;
+    }
+    if (gk && std::strcmp(gk, "twopass") == 0) return;
     size_t tile_budget = 72 * 1024;
     int kmin = 1;
     int force_row_bytes = 0;
@@ -544,7 +585,7 @@ struct otdr_dev {
 
   void ensure_partials() {
     const int seg_stripes = int((ld + tn_seg() - 1) / tn_seg());
-    const size_t need_row = size_t(std::max(std::max(stripes, gl_stripes), seg_stripes)) *
+    const size_t need_row = size_t(std::max(std::max(stripes, gl_stripes), std::max(seg_stripes, glst_groups))) *
                             size_t(std::max<long long>(m_loc, 1));
     const size_t need_col = size_t(std::max(rowgroups, num_segs * std::max(glc_k, 1))) * size_t(ld);
     const size_t need_c = size_t(cert_stripes) * size_t(num_cert_segs) * otdrk::kCertVals;

@@ -500,6 +500,157 @@ __global__ void __launch_bounds__(kThreads) gl_sweep_kernel(GLArgs<T> a) {
   }
 }
 
+// ----------------------------- group-lasso sweep, single pass (segment-staged)
+// One CTA owns a whole class segment for a narrow stripe of TN columns
+// (TN*sizeof(T) = 64 bytes: four lanes cover one row with 16-byte vectors, a
+// warp covers 8 rows per instruction). Phase 1 streams the segment's C and X
+// rows once, keeps v = [((X - rho C) + phi) + psi]_+ in shared memory and
+// accumulates the per-column ||v_g||^2; after one __syncthreads the block
+// soft-threshold scale of every column is known and phase 2 writes
+// X = v * scale from shared memory. No cluster and no re-read: 12 B per entry
+// (fp32), the segment tile (L x 64 B) limits L to the shared-memory budget.
+template <typename T, bool EXACT>
+__global__ void __launch_bounds__(512, 2) gl_stage_kernel(GLArgs<T> a, int G) {
+  using V = typename Vec<T>::type;
+  constexpr int VEC = Vec<T>::N;      // 4 floats / 2 doubles per lane
+  constexpr int TN = 64 / sizeof(T);  // 16 floats / 8 doubles: 64 B per row
+  constexpr int LPR = TN / VEC;       // lanes per row (4)
+  constexpr int RPW = 32 / LPR;       // rows per warp instruction (8)
+  constexpr int NW = 16;
+  constexpr int U = 2;                // row passes in flight
+  constexpr int ROWS_PER_PASS = NW * RPW;  // 128
+  const Ctl* ctl = a.ctl;
+  if (ctl->done) return;
+  const Segment sg = a.seg[blockIdx.y];
+  const int L = (int)(sg.end - sg.begin);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* vt = reinterpret_cast<T*>(smem_raw);                                  // L x TN staged v
+  double* rowacc = reinterpret_cast<double*>(smem_raw + (size_t)L * TN * sizeof(T));  // L
+  __shared__ double red[NW][TN];
+  __shared__ double sig[TN];
+
+  const Params& prm = *a.prm;
+  const double rho = prm.rho, thr = prm.gl_thr;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane % LPR, rsub = lane / LPR;
+  const long long group = blockIdx.x;  // this CTA sweeps stripes group*G .. group*G+G-1
+  const int ngroups = gridDim.x;
+  for (int t = threadIdx.x; t < L; t += 512) rowacc[t] = 0.0;
+
+  for (int gs = 0; gs < G; ++gs) {
+    const long long stripe = group * G + gs;
+    const long long col0 = stripe * TN + sub * VEC;
+    if (stripe * TN >= a.ld) break;  // CTA-uniform
+    const bool cok = col0 < a.ld;
+    double psi_r[VEC], sq[VEC], cacc[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      psi_r[e] = cok ? a.psi[col0 + e] : 0.0;
+      sq[e] = 0.0;
+      cacc[e] = 0.0;
+    }
+    // phase 1: v -> smem, per-column sum of v^2
+    for (int p0 = 0; p0 < L; p0 += ROWS_PER_PASS * U) {
+      V xv[U], cv[U];
+      double ph[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = p0 + u * ROWS_PER_PASS + warp * RPW + rsub;
+        if (cok && t < L) {
+          const long long i = sg.begin + t;
+          ph[u] = a.phi[i];
+          xv[u] = ld_rw(reinterpret_cast<const V*>(a.X + i * a.ld + col0));
+          cv[u] = ld_ro(reinterpret_cast<const V*>(a.C + i * a.ld + col0));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = p0 + u * ROWS_PER_PASS + warp * RPW + rsub;
+        if (cok && t < L) {
+          double x[VEC], c[VEC], o[VEC];
+          unpack(xv[u], x);
+          unpack(cv[u], c);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, c[e])), ph[u]), psi_r[e])
+                                     : (fma(-rho, c[e], x[e]) + ph[u]) + psi_r[e];
+            const double v = clamp0(val);
+            o[e] = v;
+            sq[e] += v * v;
+          }
+          reinterpret_cast<V*>(vt + (size_t)t * TN)[sub] = pack<T>(o);
+        }
+      }
+    }
+    // per-column norms: lanes sharing `sub` (xor 4, 8, 16), then warps
+#pragma unroll
+    for (int e = 0; e < VEC; ++e)
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1) sq[e] += __shfl_xor_sync(0xffffffffu, sq[e], o);
+    if (rsub == 0) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) red[warp][sub * VEC + e] = sq[e];
+    }
+    __syncthreads();
+    if (threadIdx.x < TN) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += red[w][threadIdx.x];
+      const double nrm = sqrt(s);
+      sig[threadIdx.x] = !sg.grouped ? 1.0
+                         : (nrm <= thr) ? 0.0
+                                        : (EXACT ? __dsub_rn(1.0, __ddiv_rn(thr, nrm)) : 1.0 - thr / nrm);
+    }
+    __syncthreads();
+    double sc[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) sc[e] = sig[sub * VEC + e];
+    // phase 2: X = v * scale from smem; row sums into rowacc; column sums
+    for (int t0 = 0; t0 < L; t0 += ROWS_PER_PASS) {
+      const int t = t0 + warp * RPW + rsub;
+      double rs = 0.0;
+      if (cok && t < L) {
+        const long long i = sg.begin + t;
+        double v[VEC], o[VEC];
+        unpack(reinterpret_cast<const V*>(vt + (size_t)t * TN)[sub], v);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const double nx = sg.grouped ? (EXACT ? __dmul_rn(v[e], sc[e]) : v[e] * sc[e]) : v[e];
+          o[e] = nx;
+          cacc[e] += nx;
+          rs += nx;
+        }
+        reinterpret_cast<V*>(a.X + i * a.ld)[col0 / VEC] = pack<T>(o);
+      }
+#pragma unroll
+      for (int o = 1; o < LPR; o <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+      if (sub == 0 && t < L) rowacc[t] += rs;  // one (warp, rsub) per row: no race
+    }
+#pragma unroll
+    for (int e = 0; e < VEC; ++e)
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1) cacc[e] += __shfl_xor_sync(0xffffffffu, cacc[e], o);
+    __syncthreads();  // red reused; v tile reused by the next stripe
+    if (rsub == 0) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) red[warp][sub * VEC + e] = cacc[e];
+    }
+    __syncthreads();
+    if (threadIdx.x < TN) {
+      const long long col = stripe * TN + threadIdx.x;
+      if (col < a.ld) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s += red[w][threadIdx.x];
+        a.colpart[(long long)blockIdx.y * a.ld + col] = s;
+      }
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < L; t += 512)
+    a.rowpart[(sg.begin + t) * (long long)ngroups + group] = rowacc[t];
+}
+
 // ------------------------------------- group-lasso sweep, single pass (cluster)
 // The B200 form of the group-lasso sweep. One thread-block CLUSTER of K CTAs
 // owns a (class segment, 256-byte column stripe) tile; CTA k of the cluster
