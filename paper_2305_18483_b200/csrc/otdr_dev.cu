@@ -154,6 +154,10 @@ struct otdr_dev {
   // segment-staged GL sweep: one CTA per (segment, group of glst_g stripes)
   int glst_g = 0, glst_groups = 0;
   size_t glst_smem = 0;
+  // TMA box-ring GL sweep: one CTA per (segment, group of glr_g stripes)
+  int glr_g = 0, glr_groups = 0, glr_nb = 0;
+  size_t glr_smem = 0;
+  CUtensorMap glr_mapX{}, glr_mapC{};
   // TMA-pipelined plain sweep (OTDR_SWEEP=tma): box 256 cols x kSweepTR rows
   bool use_tma_sweep = false;
   CUtensorMap sw_mapX{}, sw_mapC{};
@@ -220,12 +224,32 @@ struct otdr_dev {
 
   // The cluster kernel covers the plain (non-fused, untracked) iteration; the
   // even/odd and support-tracking variants use the two-phase kernel.
-  bool gl_stage_active(bool track) const { return glst_g > 0 && !track && !prm.fused; }
+  bool gl_ring_active(bool track) const { return glr_g > 0 && !track && !prm.fused; }
+  bool gl_stage_active(bool track) const {
+    return !gl_ring_active(track) && glst_g > 0 && !track && !prm.fused;
+  }
   bool gl_cluster_active(bool track) const {
     return !gl_stage_active(track) && glc_tn > 0 && !track && !prm.fused;
   }
 
   void launch_sweep(bool track, bool sums_only) {
+    if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only && gl_ring_active(track)) {
+      const dim3 grid{unsigned(glr_groups), unsigned(num_segs), 1u};
+      if (f64()) {
+        otdrk::GLArgs<double> ga{(double*)X, (const double*)C, phi, psi, rowpart, colpart,
+                                 d_seg, d_prm, d_ctl, m_loc, ld};
+        CK(cudaFuncSetAttribute(otdrk::gl_ring_kernel<double, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(glr_smem)));
+        otdrk::gl_ring_kernel<double, true><<<grid, 512, glr_smem, stream>>>(ga, glr_mapX, glr_mapC, glr_g, glr_nb);
+      } else {
+        otdrk::GLArgs<float> ga{(float*)X, (const float*)C, phi, psi, rowpart, colpart,
+                                d_seg, d_prm, d_ctl, m_loc, ld};
+        CK(cudaFuncSetAttribute(otdrk::gl_ring_kernel<float, false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(glr_smem)));
+        otdrk::gl_ring_kernel<float, false><<<grid, 512, glr_smem, stream>>>(ga, glr_mapX, glr_mapC, glr_g, glr_nb);
+      }
+      return;
+    }
     if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only && gl_stage_active(track)) {
       const dim3 grid{unsigned(glst_groups), unsigned(num_segs), 1u};
       if (f64()) {
@@ -329,6 +353,7 @@ struct otdr_dev {
   // by the sweep variant that runs in this configuration.
   std::pair<int, int> partial_shape(bool sums_only, bool track) const {
     if (gl_active(sums_only)) {
+      if (gl_ring_active(track)) return {glr_groups, num_segs};
       if (gl_stage_active(track)) return {glst_groups, num_segs};
       if (gl_cluster_active(track)) return {gl_stripes, num_segs * glc_k};
       return {int((ld + tn_seg() - 1) / tn_seg()), num_segs};
@@ -532,6 +557,10 @@ struct otdr_dev {
     glst_g = 0;
     glst_groups = 0;
     glst_smem = 0;
+    glr_g = 0;
+    glr_groups = 0;
+    glr_nb = 0;
+    glr_smem = 0;
     if (reg_kind != OTDR_REG_GROUP_LASSO || m_loc == 0) return;
     long long lmax = 0;
     for (const Segment& sg : segs) lmax = std::max(lmax, sg.end - sg.begin);
@@ -540,7 +569,19 @@ struct otdr_dev {
     // shared memory (<= 100 KB: two or three CTAs per SM); OTDR_GL_KERNEL
     // selects stage / cluster / twopass explicitly.
     const char* gk = std::getenv("OTDR_GL_KERNEL");
+    const bool want_ring = !gk || std::strcmp(gk, "ring") == 0;
     const bool want_stage = !gk || std::strcmp(gk, "stage") == 0;
+    if (want_ring && lmax <= 1024) {
+      const long long tn = 64 / (long long)esz;
+      const long long nstr = (ld + tn - 1) / tn;
+      glr_nb = int((lmax + 255) / 256);
+      const long long work = nstr * (long long)num_segs;
+      glr_g = int(std::max<long long>(1, (work + 4LL * num_sms - 1) / (4LL * num_sms)));
+      glr_groups = int((nstr + glr_g - 1) / glr_g);
+      glr_smem = 2 * size_t(glr_nb) * 256 * 64 + size_t(glr_nb) * 256 * 8 + 2 * size_t(glr_nb) * 8;
+      encode_map(&glr_mapX, X, int(tn), 256);
+      encode_map(&glr_mapC, C, int(tn), 256);
+    }
     const size_t stage_bytes = size_t(lmax) * (64 + 8);
     if (want_stage && stage_bytes <= size_t(100) * 1024) {
       const long long tn = 64 / (long long)esz;
@@ -585,7 +626,7 @@ struct otdr_dev {
 
   void ensure_partials() {
     const int seg_stripes = int((ld + tn_seg() - 1) / tn_seg());
-    const size_t need_row = size_t(std::max(std::max(stripes, gl_stripes), std::max(seg_stripes, glst_groups))) *
+    const size_t need_row = size_t(std::max(std::max(std::max(stripes, gl_stripes), std::max(seg_stripes, glst_groups)), glr_groups)) *
                             size_t(std::max<long long>(m_loc, 1));
     const size_t need_col = size_t(std::max(rowgroups, num_segs * std::max(glc_k, 1))) * size_t(ld);
     const size_t need_c = size_t(cert_stripes) * size_t(num_cert_segs) * otdrk::kCertVals;

@@ -1007,6 +1007,196 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_tma_kernel(SweepArgs<T> a,
   }
 }
 
+// ------------------------------ group-lasso sweep, single pass (TMA box ring)
+// Segment-staged like gl_stage_kernel, but C and X arrive as 2-D TMA boxes
+// (64 B x 256 rows) into per-box shared-memory buffers with mbarrier
+// completion, and every buffer is refilled for the NEXT stripe as soon as it
+// is consumed: a C box right after phase 1 used it, an X box (holding v) right
+// after phase 2 wrote it back. HBM therefore streams continuously while the
+// CTA alternates between the norm phase and the scaling phase.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <typename T, bool EXACT>
+__global__ void __launch_bounds__(512, 1) gl_ring_kernel(GLArgs<T> a,
+                                                        const __grid_constant__ CUtensorMap mapX,
+                                                        const __grid_constant__ CUtensorMap mapC,
+                                                        int G, int NB) {
+  using V = typename Vec<T>::type;
+  constexpr int VEC = Vec<T>::N;
+  constexpr int TN = 64 / sizeof(T);
+  constexpr int LPR = TN / VEC;            // 4 lanes per row
+  constexpr int RPW = 32 / LPR;            // 8 rows per warp instruction
+  constexpr int NW = 16;
+  constexpr int BR = 256;                  // rows per TMA box
+  constexpr unsigned kBox = BR * 64;       // bytes per box
+  const Ctl* ctl = a.ctl;
+  if (ctl->done) return;
+  const Segment sg = a.seg[blockIdx.y];
+  const int L = (int)(sg.end - sg.begin);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* xb = reinterpret_cast<T*>(smem_raw);                         // NB boxes (X, then v)
+  T* cb = reinterpret_cast<T*>(smem_raw + (size_t)NB * kBox);     // NB boxes (C)
+  double* rowacc = reinterpret_cast<double*>(smem_raw + 2 * (size_t)NB * kBox);  // NB*BR
+  unsigned long long* fx = reinterpret_cast<unsigned long long*>(rowacc + (size_t)NB * BR);
+  unsigned long long* fc = fx + NB;
+  __shared__ double red[NW][TN];
+  __shared__ double sig[TN];
+
+  const Params& prm = *a.prm;
+  const double rho = prm.rho, thr = prm.gl_thr;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane % LPR, rsub = lane / LPR;
+  const long long group = blockIdx.x;
+  const int ngroups = gridDim.x;
+  int nstr = G;
+  {
+    const long long first = group * G;
+    const long long total = (a.ld + TN - 1) / TN;
+    if (first + nstr > total) nstr = (int)(total - first);
+  }
+  const int nbox = (L + BR - 1) / BR;
+  auto issue = [&](const CUtensorMap* map, T* buf, unsigned long long* bar, long long stripe, int kb) {
+    mbar_expect_tx(bar, kBox);
+    tma_load_2d(buf, map, (int)(stripe * TN), (int)(sg.begin + (long long)kb * BR), bar);
+  };
+  if (threadIdx.x == 0) {
+    for (int kb = 0; kb < NB; ++kb) {
+      mbar_init(&fx[kb], 1);
+      mbar_init(&fc[kb], 1);
+    }
+    if (nstr > 0)
+      for (int kb = 0; kb < nbox; ++kb) {
+        issue(&mapX, xb + (size_t)kb * BR * TN, &fx[kb], group * G, kb);
+        issue(&mapC, cb + (size_t)kb * BR * TN, &fc[kb], group * G, kb);
+      }
+  }
+  for (int t = threadIdx.x; t < nbox * BR; t += 512) rowacc[t] = 0.0;
+  __syncthreads();
+
+  for (int si = 0; si < nstr; ++si) {
+    const long long stripe = group * G + si;
+    const bool has_next = si + 1 < nstr;
+    const unsigned par = (unsigned)(si & 1);
+    const long long col0 = stripe * TN + sub * VEC;
+    const bool cok = col0 < a.ld;
+    double psi_r[VEC], sq[VEC], cacc[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      psi_r[e] = cok ? a.psi[col0 + e] : 0.0;
+      sq[e] = 0.0;
+      cacc[e] = 0.0;
+    }
+    // phase 1, box by box
+    for (int kb = 0; kb < nbox; ++kb) {
+      mbar_wait(&fx[kb], par);
+      mbar_wait(&fc[kb], par);
+      T* xt = xb + (size_t)kb * BR * TN;
+      const T* ct = cb + (size_t)kb * BR * TN;
+#pragma unroll
+      for (int pass = 0; pass < BR / (NW * RPW); ++pass) {
+        const int r = pass * NW * RPW + warp * RPW + rsub;  // row within the box
+        const int t = kb * BR + r;                          // row within the segment
+        if (cok && t < L) {
+          const double ph = a.phi[sg.begin + t];
+          double x[VEC], c[VEC], o[VEC];
+          unpack(reinterpret_cast<const V*>(xt + (size_t)r * TN)[sub], x);
+          unpack(reinterpret_cast<const V*>(ct + (size_t)r * TN)[sub], c);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, c[e])), ph), psi_r[e])
+                                     : (fma(-rho, c[e], x[e]) + ph) + psi_r[e];
+            const double v = clamp0(val);
+            o[e] = v;
+            sq[e] += v * v;
+          }
+          reinterpret_cast<V*>(xt + (size_t)r * TN)[sub] = pack<T>(o);
+        }
+      }
+      __syncthreads();  // C box kb consumed by every thread
+      if (threadIdx.x == 0 && has_next) {
+        fence_proxy_async_smem();
+        issue(&mapC, cb + (size_t)kb * BR * TN, &fc[kb], stripe + 1, kb);
+      }
+    }
+    // per-column norms
+#pragma unroll
+    for (int e = 0; e < VEC; ++e)
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1) sq[e] += __shfl_xor_sync(0xffffffffu, sq[e], o);
+    if (rsub == 0) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) red[warp][sub * VEC + e] = sq[e];
+    }
+    __syncthreads();
+    if (threadIdx.x < TN) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += red[w][threadIdx.x];
+      const double nrm = sqrt(s);
+      sig[threadIdx.x] = !sg.grouped ? 1.0
+                         : (nrm <= thr) ? 0.0
+                                        : (EXACT ? __dsub_rn(1.0, __ddiv_rn(thr, nrm)) : 1.0 - thr / nrm);
+    }
+    __syncthreads();
+    double sc[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) sc[e] = sig[sub * VEC + e];
+    // phase 2, box by box; each X box is refilled with the next stripe once written back
+    for (int kb = 0; kb < nbox; ++kb) {
+      const T* vt = xb + (size_t)kb * BR * TN;
+#pragma unroll
+      for (int pass = 0; pass < BR / (NW * RPW); ++pass) {
+        const int r = pass * NW * RPW + warp * RPW + rsub;
+        const int t = kb * BR + r;
+        double rs = 0.0;
+        if (cok && t < L) {
+          double v[VEC], o[VEC];
+          unpack(reinterpret_cast<const V*>(vt + (size_t)r * TN)[sub], v);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const double nx = sg.grouped ? (EXACT ? __dmul_rn(v[e], sc[e]) : v[e] * sc[e]) : v[e];
+            o[e] = nx;
+            cacc[e] += nx;
+            rs += nx;
+          }
+          reinterpret_cast<V*>(a.X + (sg.begin + t) * a.ld)[col0 / VEC] = pack<T>(o);
+        }
+#pragma unroll
+        for (int o = 1; o < LPR; o <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+        if (sub == 0 && t < L) rowacc[t] += rs;
+      }
+      __syncthreads();  // X box kb written back by every thread
+      if (threadIdx.x == 0 && has_next) {
+        fence_proxy_async_smem();  // generic writes of v before the async-proxy refill
+        issue(&mapX, xb + (size_t)kb * BR * TN, &fx[kb], stripe + 1, kb);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < VEC; ++e)
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1) cacc[e] += __shfl_xor_sync(0xffffffffu, cacc[e], o);
+    if (rsub == 0) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) red[warp][sub * VEC + e] = cacc[e];
+    }
+    __syncthreads();
+    if (threadIdx.x < TN) {
+      const long long col = stripe * TN + threadIdx.x;
+      if (col < a.ld) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s += red[w][threadIdx.x];
+        a.colpart[(long long)blockIdx.y * a.ld + col] = s;
+      }
+    }
+    __syncthreads();  // red reused by the next stripe
+  }
+  for (int t = threadIdx.x; t < L; t += 512)
+    a.rowpart[(sg.begin + t) * (long long)ngroups + group] = rowacc[t];
+}
+
 // ---------------------------------------------------------------- reduce
 // Blocks [0, RB): rows. R_i = sum_s rowpart[s][i] (stripe order), r_i = R_i - p_i,
 // block partials (sum r, sum r^2, sum R); the last row block folds them in

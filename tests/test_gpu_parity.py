@@ -371,13 +371,17 @@ def test_large_fp32_properties(ora):
     np.testing.assert_allclose(g.X.sum(axis=1) - p, g.r, atol=1e-9)
 
 
+@pytest.mark.parametrize("kernel", ["auto", "ring", "stage", "cluster", "twopass"])
 @pytest.mark.parametrize("storage,m,n,classes", [
-    ("f64", 3000, 300, 2),    # cluster of 8 CTAs per class segment (DSMEM norms)
+    ("f64", 3000, 300, 2),    # long segments: cluster of 8 CTAs (DSMEM norms)
     ("f32", 3000, 301, 2),
     ("f32", 1000, 1000, 10),  # the cfg3 shape at 1/10 scale
-    ("f64", 4000, 64, 1),     # segment too long for a cluster: two-phase fallback
+    ("f64", 2000, 203, 2),    # 1000-row segments: TMA box ring / segment-staged
+    ("f64", 4000, 64, 1),     # segment too long for any staging: two-phase fallback
 ])
-def test_gl_long_segments_match_oracle(ora, storage, m, n, classes):
+def test_gl_long_segments_match_oracle(ora, monkeypatch, kernel, storage, m, n, classes):
+    if kernel != "auto":
+        monkeypatch.setenv("OTDR_GL_KERNEL", kernel)
     C, p, q, src, tgt, ls, lt = ora.adaptation_problem(m, n, classes, 3)
     Co = C if storage == "f64" else C.astype(np.float32).astype(np.float64)
     pr = ora.Problem(Co, p, q)
