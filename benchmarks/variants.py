@@ -1,0 +1,69 @@
+#!/usr/bin/env python
+"""Compare sweep-kernel variants (selected by environment variables, read at
+Engine creation) on one config; one JSON line per variant.
+
+  python benchmarks/variants.py headline OTDR_SWEEP=default OTDR_SWEEP=tma
+  python benchmarks/variants.py cfg3 OTDR_GL_KERNEL=ring OTDR_GL_KERNEL=stage OTDR_GL_PLAN=off
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import json, os, sys
+sys.path.insert(0, ROOT)
+import torch
+import paper_2305_18483_b200 as otdr
+from paper_2305_18483_b200 import datagen
+cfg = CFG
+if cfg in ("headline", "cfg2", "cfg4"):
+    m = {"headline": 20000, "cfg2": 10000, "cfg4": 40000}[cfg]
+    reg = {"headline": otdr.QuadraticReg(200.0), "cfg2": otdr.ZeroReg(), "cfg4": otdr.QuadraticReg(400.0)}[cfg]
+    eng = otdr.Engine(m, m, "f32")
+    src, tgt = datagen.gaussian_points(m, m, 0)
+    eng.build_sqdist_cost(src, tgt, datagen.uniform(m), datagen.uniform(m))
+else:
+    m = 10000
+    src, tgt, ls, lt = datagen.adaptation_points(m, m, 10, 0)
+    eng = otdr.Engine(m, m, "f32")
+    eng.build_sqdist_cost(src, tgt, datagen.uniform(m), datagen.uniform(m))
+    reg = otdr.GroupLassoReg(1e-3, otdr.column_class_blocks(ls, m))
+eng.set_regularizer(reg)
+eng.set_state()
+rho = otdr.default_stepsize(m, m)
+eng.step(rho, 5)
+ms = eng.time_steps(rho, ITERS) / ITERS
+prof = eng.profile(rho, 5)
+alg = 12.0 * m * m
+print("RESULT " + json.dumps(dict(cfg=cfg, variant=VARIANT, ms_per_iter=ms, iters_per_s=1e3 / ms,
+      sweep_ms=prof["sweep_ms"], sweep_GBps=alg / prof["sweep_ms"] / 1e6,
+      iter_GBps=alg / ms / 1e6, prof=prof)), flush=True)
+"""
+
+
+def main():
+    cfg = sys.argv[1]
+    iters = 100 if cfg != "cfg4" else 30
+    for var in sys.argv[2:] or ["default"]:
+        env = dict(os.environ)
+        for kv in var.split(","):
+            if "=" in kv:
+                k, v = kv.split("=", 1)
+                env[k] = v
+        code = CHILD.replace("ROOT", repr(ROOT)).replace("CFG", repr(cfg)) \
+                    .replace("ITERS", str(iters)).replace("VARIANT", repr(var))
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+        got = [l[7:] for l in out.stdout.splitlines() if l.startswith("RESULT ")]
+        if got:
+            print(got[0], flush=True)
+        else:
+            print(json.dumps(dict(cfg=cfg, variant=var, error=(out.stderr or out.stdout)[-800:])), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -9,6 +9,7 @@
 #include "otdr_dev.h"
 #include "otdr_kernels.cuh"
 #include "otdr_resident.cuh"
+#include "otdr_stream.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -126,6 +127,14 @@ struct otdr_dev {
   int res_G = 0, res_R = 0;
   size_t res_smem = 0;
   double* gscratch = nullptr;
+  // persistent streaming solve (single GPU, zero / quadratic, HBM-resident plan)
+  bool allow_stream = true;
+  int str_P = 0, str_ntiles = 0, str_tpc = 8, str_tail = 2;
+  double *str_part = nullptr, *str_colpart = nullptr;
+  int4* d_tiles = nullptr;
+  int* d_sfirst = nullptr;
+  unsigned* d_scnt = nullptr;
+  double* str_sspart = nullptr;
   long long* d_dev_row = nullptr;
   Segment *d_seg = nullptr, *d_cert_seg = nullptr;
   Params* d_prm = nullptr;
@@ -482,6 +491,7 @@ struct otdr_dev {
     num_cert_segs = int(cert_segs.size());
     plan_gl_cluster();
     plan_resident();
+    plan_stream();
     if (use_tma_sweep && m_loc > 0) {
       encode_map(&sw_mapX, X, 256, kSweepTR);
       encode_map(&sw_mapC, C, 256, kSweepTR);
@@ -514,6 +524,150 @@ struct otdr_dev {
     res_R = int(R);
     res_smem = bytes;
     if (!gscratch) gscratch = dalloc<double>(size_t(num_sms) * size_t(n + 4));
+  }
+
+  // Streaming plan: P co-resident CTAs claiming (row group, stripe) tiles of
+  // the plain sweep's geometry (rows_per_cta x 256 columns).
+  void plan_stream() {
+    str_P = 0;
+    if (!allow_stream || sharded || m_loc < 1 || reg_kind == OTDR_REG_GROUP_LASSO) return;
+    int occ = 0;
+    if (str_d < 0) str_d = default_stream_d();
+    cudaLaunchConfig_t lc{};
+    stream_dispatch(lc, otdrk::StreamArgs{}, &occ);
+    if (occ < 1) return;
+    const long long P = (long long)num_sms * occ;
+    const long long S = (ld + otdrk::kStreamTN - 1) / otdrk::kStreamTN;
+    // long tiles (the plain sweep's rows_per_cta), short ones for the last
+    // stripes, about two rounds of long tiles' worth of rows
+    // about str_tpc long tiles per CTA (OTDR_STREAM_TILES)
+    const long long big = std::max<long long>(16, (m_loc * S + str_tpc * P - 1) / (str_tpc * P));
+    const long long small = std::max<long long>(32, big / std::max(1, str_tail));
+    const long long tail_stripes =
+        str_tail > 1 ? std::min<long long>(S, (P * big + m_loc - 1) / m_loc) : 0;
+    std::vector<int4> tiles;
+    std::vector<int> first;
+    for (long long st = 0; st < S; ++st) {
+      first.push_back(int(tiles.size()));
+      const long long R = st >= S - tail_stripes ? small : big;
+      for (long long r0 = 0; r0 < m_loc; r0 += R)
+        tiles.push_back(int4{int(st), int(r0), int(std::min(m_loc, r0 + R)), 0});
+    }
+    first.push_back(int(tiles.size()));
+    for (void* ptr : {(void*)str_part, (void*)str_colpart, (void*)d_tiles, (void*)d_sfirst,
+                      (void*)d_scnt, (void*)str_sspart})
+      if (ptr) cudaFree(ptr);
+    d_scnt = dalloc<unsigned>(size_t(S));
+    CK(cudaMemset(d_scnt, 0, size_t(S) * sizeof(unsigned)));
+    str_sspart = dalloc<double>(size_t(S));
+    str_part = dalloc<double>(size_t(P) * 4);
+    str_colpart = dalloc<double>(tiles.size() * otdrk::kStreamTN);
+    d_tiles = dalloc<int4>(tiles.size());
+    d_sfirst = dalloc<int>(first.size());
+    CK(cudaMemcpy(d_tiles, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_sfirst, first.data(), first.size() * sizeof(int), cudaMemcpyHostToDevice));
+    str_ntiles = int(tiles.size());
+    str_P = int(P);
+  }
+
+  // cp.async queue depth (rows in flight per warp, OTDR_STREAM_D); 0 = register-staged sweep
+  int str_d = -1;
+  int default_stream_d() const { return f64() ? 3 : 4; }
+  template <typename T, int REG, int D>
+  static constexpr size_t stream_smem_of() {
+    return D > 0 ? otdrk::stream_async_smem<T, sizeof(T) == 8 ? 4 : 2, D>() : 0;
+  }
+  template <typename T, int REG, int D>
+  void stream_call(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
+    constexpr bool E = sizeof(T) == 8;
+    constexpr int NV = E ? 4 : 2, U = E ? 1 : 2;
+    auto kern = otdrk::stream_kernel<T, REG, E, NV, U, D>;
+    const size_t smem = stream_smem_of<T, REG, D>();
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    if (occ) {
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, otdrk::kThreads, smem));
+      return;
+    }
+    lc.dynamicSmemBytes = smem;
+    CK(cudaLaunchKernelEx(&lc, kern, sa));
+  }
+  template <typename T, int REG>
+  void stream_dispatch_d(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
+    switch (str_d) {
+      case 0: stream_call<T, REG, 0>(lc, sa, occ); break;
+      case 2: stream_call<T, REG, 2>(lc, sa, occ); break;
+      case 3: stream_call<T, REG, 3>(lc, sa, occ); break;
+      case 4: stream_call<T, REG, 4>(lc, sa, occ); break;
+      default: stream_call<T, REG, 5>(lc, sa, occ); break;
+    }
+  }
+  void stream_dispatch(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
+    const bool quad = reg_kind == OTDR_REG_QUAD;
+    if (f64()) {
+      if (quad) stream_dispatch_d<double, otdrk::REG_QUAD>(lc, sa, occ);
+      else stream_dispatch_d<double, otdrk::REG_NONE>(lc, sa, occ);
+    } else {
+      if (quad) stream_dispatch_d<float, otdrk::REG_QUAD>(lc, sa, occ);
+      else stream_dispatch_d<float, otdrk::REG_NONE>(lc, sa, occ);
+    }
+  }
+
+  bool stream_active(bool track, bool cert) const {
+    return str_P > 0 && res_G == 0 && !track && !cert && !prm.fused;
+  }
+
+  void launch_stream(long long iters) {
+    const long long S = (ld + otdrk::kStreamTN - 1) / otdrk::kStreamTN;
+    otdrk::StreamArgs sa{X, C, phi, a, r, p, psi, b, s, q, rowpart, str_colpart, d_tiles,
+                         d_sfirst, d_scnt, str_sspart, str_part, d_ctl, d_prm, m_loc, n, ld, int(S), str_ntiles,
+                         iters, nullptr};
+    static const bool trace = std::getenv("OTDR_STREAM_TRACE") != nullptr;
+    unsigned long long* ts = nullptr;
+    const size_t tsn = size_t(otdrk::kTraceIters) * size_t(str_P + 8);
+    if (trace) {
+      ts = dalloc<unsigned long long>(tsn);
+      CK(cudaMemset(ts, 0, tsn * 8));
+      sa.tstamp = ts;
+    }
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(unsigned(str_P), 1, 1);
+    lc.blockDim = dim3(otdrk::kThreads, 1, 1);
+    lc.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    stream_dispatch(lc, sa, nullptr);
+    if (trace) {  // debug: per-iteration phase times of the first iterations
+      std::vector<unsigned long long> h(tsn);
+      CK(cudaStreamSynchronize(stream));
+      CK(cudaMemcpy(h.data(), ts, tsn * 8, cudaMemcpyDeviceToHost));
+      cudaFree(ts);
+      for (int it = 0; it < otdrk::kTraceIters; ++it) {
+        const unsigned long long* row = h.data() + size_t(it) * size_t(str_P + 8);
+        const unsigned long long t0 = row[str_P];
+        if (!t0) break;
+        unsigned long long mn = ~0ull, mx = 0;
+        for (int c = 0; c < str_P; ++c) {
+          mn = std::min(mn, row[c]);
+          mx = std::max(mx, row[c]);
+        }
+        std::fprintf(stderr,
+                     "stream it %d: sweep first %.1f last %.1f us | bar1 %.1f | rows %.1f cols %.1f | B %.1f | bar2 %.1f | C %.1f\n",
+                     it, (mn - t0) * 1e-3, (mx - t0) * 1e-3, (row[str_P + 1] - t0) * 1e-3,
+                     (row[str_P + 5] - t0) * 1e-3, (row[str_P + 6] - t0) * 1e-3,
+                     (row[str_P + 2] - t0) * 1e-3, (row[str_P + 3] - t0) * 1e-3,
+                     (row[str_P + 4] - t0) * 1e-3);
+        if (it == 1) {
+          std::vector<double> dv(static_cast<size_t>(str_P));
+          for (int c = 0; c < str_P; ++c) dv[size_t(c)] = (row[c] - t0) * 1e-3;
+          std::fprintf(stderr, "  per-CTA sweep end (us):");
+          for (int c = 0; c < str_P; ++c) std::fprintf(stderr, " %.0f", dv[size_t(c)]);
+          std::fprintf(stderr, "\n");
+        }
+      }
+    }
   }
 
   bool resident_active(bool track, bool cert) const {
@@ -717,6 +871,11 @@ struct otdr_dev {
       check_launch();
       return;
     }
+    if (iters > 0 && stream_active(false, false)) {
+      launch_stream(iters);
+      check_launch();
+      return;
+    }
     const int chunk = 16;
     if (iters >= chunk) {
       cudaGraphExec_t ex = get_graph(0, chunk, false, false);
@@ -814,6 +973,7 @@ struct otdr_dev {
   void release() {
     invalidate_graphs();
     void* ptrs[] = {C, X, p, q, phi, psi, a, b, r, s, rowpart, colpart, exch, bpart, cpart,
+                    str_part, str_colpart, d_tiles, d_sfirst, d_scnt, str_sspart,
                     csum, stage, fpart, fpart2, gscratch, d_dev_row, d_seg, d_cert_seg, d_prm, d_ctl, d_trace, d_mx};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);
@@ -905,7 +1065,7 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     CK(cudaMemset(ctx->X, 0, mat));
     const size_t ml = size_t(std::max<long long>(ctx->m_loc, 1));
     ctx->p = dalloc<double>(ml);
-    ctx->phi = dalloc<double>(ml);
+    ctx->phi = dalloc<double>(ml + 1);  // +1: 16-byte cp.async of phi pairs
     ctx->a = dalloc<double>(ml);
     ctx->r = dalloc<double>(ml);
     ctx->q = dalloc<double>(size_t(ctx->ld));
@@ -920,6 +1080,11 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     if (const char* fe = std::getenv("OTDR_FINALIZE")) ctx->use_fused_finalize = std::strcmp(fe, "fused") == 0;
     if (const char* re = std::getenv("OTDR_RESIDENT")) ctx->allow_resident = std::strcmp(re, "off") != 0;
     if (const char* se = std::getenv("OTDR_SWEEP")) ctx->use_tma_sweep = std::strcmp(se, "tma") == 0;
+    if (const char* st = std::getenv("OTDR_STREAM")) ctx->allow_stream = std::strcmp(st, "off") != 0;
+    ctx->str_d = -1;
+    if (const char* tp = std::getenv("OTDR_STREAM_TILES")) ctx->str_tpc = std::max(1, std::atoi(tp));
+    if (const char* tl = std::getenv("OTDR_STREAM_TAIL")) ctx->str_tail = std::max(1, std::atoi(tl));
+    if (const char* sd = std::getenv("OTDR_STREAM_D")) ctx->str_d = std::atoi(sd);
     {
       int occ = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, otdrk::finalize_kernel,
@@ -1303,7 +1468,8 @@ otdr_status otdr_dev_time_steps(otdr_dev* ctx, double rho, int64_t iters, double
     ctx->prm.fused = 0;
     ctx->prm.record_trace = 0;
     ctx->push_prm();
-    if (iters >= 16) ctx->get_graph(0, 16, false, false);  // instantiate outside the timing
+    if (iters >= 16 && !ctx->stream_active(false, false) && !ctx->resident_active(false, false))
+      ctx->get_graph(0, 16, false, false);  // instantiate outside the timing
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaEventRecord(ctx->ev0, ctx->stream));
     ctx->run_raw(iters);
@@ -1422,15 +1588,19 @@ otdr_status otdr_dev_solve(otdr_dev* ctx, const otdr_solve_opts* o, otdr_solve_r
     // sweep compares each entry's old and new sign.
     CK(cudaStreamSynchronize(ctx->stream));
     const bool resident = ctx->resident_active(track, cert);
+    const bool streaming = !resident && ctx->stream_active(track, cert);
     const bool use_while = ctx->comm == nullptr;
     const int body = 4;
     cudaGraphExec_t ex = nullptr;
-    if (!resident)
+    if (!resident && !streaming)
       ex = use_while ? ctx->get_graph(1, body, track, cert) : ctx->get_graph(0, 8, track, cert);
     CK(cudaEventRecord(ctx->ev0, ctx->stream));
     otdrk::stamp_t0_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_ctl);
     if (resident) {
       ctx->launch_resident(0);
+      ctx->check_launch();
+    } else if (streaming) {
+      ctx->launch_stream(0);
       ctx->check_launch();
     } else if (use_while) {
       CK(cudaGraphLaunch(ex, ctx->stream));

@@ -78,6 +78,9 @@ struct Ctl {
   // always holds a multiple of that grid size.
   unsigned long long bar_fin;  // cooperative finalize kernel
   unsigned long long bar_res;  // resident solve kernel
+  unsigned long long bar_str;  // streaming solve kernel
+  unsigned int tile_ctr;       // streaming kernel: tiles claimed this sweep
+  unsigned int pad_;
 };
 
 struct TraceRow {

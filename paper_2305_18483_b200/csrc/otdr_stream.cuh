@@ -1,0 +1,501 @@
+// otdr_stream.cuh -- persistent streaming solve loop for plans that live in
+// HBM (single GPU, zero / quadratic regularizer).
+//
+// One cooperative launch runs many DR iterations (solver.cpp:95-102 + :23-38):
+// every CTA of a co-resident grid (P = SMs x CTAs/SM) owns a fixed, equal
+// share of the plan for the whole solve, so there are no per-iteration
+// launches, no wave tail and no separate reduce/update kernels.
+//
+// Work split. The plan is cut into tiles of rows x 256 columns, numbered
+// stripe-major (all row ranges of stripe 0, then stripe 1, ...); the last
+// stripes use short tiles so the sweep ends with a fine-grained tail. CTAs
+// claim tiles from a per-iteration atomic counter: a static equal split was
+// measured to leave a 350 us spread of CTA finish times per sweep on B200 at
+// 20000^2, dynamic claiming lets fast CTAs take more tiles.
+//
+// One iteration:
+//   A  sweep own segments: X <- prox([((X - rho C) + phi_i) + psi_j]_+),
+//      row partials rowpart[row][stripe] (warp butterfly), column partials per
+//      tile in registers -> fixed-order cross-warp smem sum -> colpart[tile]
+//      (one slot per tile: the fold order does not depend on which CTA swept it)
+//   -- grid barrier --
+//      the CTA completing a stripe's last tile folds its column partials
+//      (tile order): s = S - q and the stripe's sum of s^2
+//   B  row folds (warp per row, stripe order): r = R - p, partial sums of r,
+//      r^2, R; one (sr, sr2, sR) record per CTA
+//   -- grid barrier --
+//   C  every CTA folds the P records in the same fixed order -> identical eta,
+//      shift, r_primal and stopping decision everywhere; phi/a (thread per
+//      row), psi/b (thread per column); the solve loop's stopping logic
+//      (solver.cpp:179-235)
+//   -- grid barrier (only when continuing) --
+// Cross-CTA data (phi, psi, r, partials) is read with ld.global.cg (L2), so
+// no stale L1 line survives a barrier; X and C tiles are owned by one CTA.
+#pragma once
+#include "otdr_kernels.cuh"
+
+namespace otdrk {
+
+struct StreamArgs {
+  void* X;
+  const void* C;
+  double* phi;
+  double* a;
+  double* r;
+  const double* p;
+  double* psi;
+  double* b;
+  double* s;
+  const double* q;
+  double* rowpart;        // [m][stripes]
+  double* colpart;        // [ntiles][TN] one slot per tile
+  const int4* tiles;      // [ntiles] {stripe, row begin, row end, -}, stripe-major
+  const int* sfirst;      // [stripes + 1] first tile of each stripe
+  unsigned* scnt;         // [stripes] tiles completed this sweep (zero between sweeps)
+  double* sspart;         // [stripes] sum of s_j^2 over the stripe's columns
+  double* part;           // [P][4]
+  Ctl* ctl;
+  const Params* prm;
+  long long m, n, ld;
+  int stripes, ntiles;
+  long long iters;        // raw mode (prm.solving == 0): iterations to run
+  unsigned long long* tstamp;  // optional phase timestamps [kTraceIters][P + 8] (debug)
+};
+constexpr int kTraceIters = 4;
+
+constexpr int kStreamTN = 256;
+
+template <typename T, int REG, bool EXACT, int NV, int U>
+__device__ __forceinline__ void stream_segment(const StreamArgs& A, int tile, long long stripe,
+                                               long long r0, long long r1, double rho, double qd,
+                                               double qinv, double (*red)[kStreamTN]) {
+  using V = typename Vec<T>::type;
+  constexpr int VEC = Vec<T>::N;
+  static_assert(32 * VEC * NV == kStreamTN, "stripe width");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T* X = static_cast<T*>(A.X);
+  const T* C = static_cast<const T*>(A.C);
+  const long long col0 = stripe * kStreamTN;
+  long long cols[NV];
+  bool cok[NV];
+  double psi_r[NV][VEC], cacc[NV][VEC];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    cols[v] = col0 + v * 32 * VEC + lane * VEC;
+    cok[v] = cols[v] < A.ld;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      psi_r[v][e] = cok[v] ? __ldcg(A.psi + cols[v] + e) : 0.0;
+      cacc[v][e] = 0.0;
+    }
+  }
+  for (long long i0 = r0 + warp; i0 < r1; i0 += (long long)kWarps * U) {
+    V xv[U][NV], cv[U][NV];
+    double phv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + (long long)u * kWarps;
+      if (i < r1) {
+        phv[u] = __ldcg(A.phi + i);
+        const V* xrow = reinterpret_cast<const V*>(X + i * A.ld);
+        const V* crow = reinterpret_cast<const V*>(C + i * A.ld);
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+          if (cok[v]) {
+            xv[u][v] = ld_rw(xrow + cols[v] / VEC);
+            cv[u][v] = ld_ro(crow + cols[v] / VEC);
+          }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + (long long)u * kWarps;
+      if (i >= r1) break;  // warp-uniform
+      double rs = 0.0;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        if (!cok[v]) continue;
+        double x[VEC], cc[VEC], o[VEC];
+        unpack(xv[u][v], x);
+        unpack(cv[u][v], cc);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          // ((X - rho C) + phi) + psi, clamp (solver.cpp:97-99), prox
+          const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, cc[e])), phv[u]),
+                                               psi_r[v][e])
+                                   : (fma(-rho, cc[e], x[e]) + phv[u]) + psi_r[v][e];
+          double nx = clamp0(val);
+          if (REG == REG_QUAD) nx = EXACT ? __ddiv_rn(nx, qd) : nx * qinv;  // regularizers.cpp:54
+          o[e] = nx;
+          cacc[v][e] += nx;
+          rs += nx;
+        }
+        reinterpret_cast<V*>(X + i * A.ld)[cols[v] / VEC] = pack<T>(o);
+      }
+      rs = warp_sum(rs);
+      if (lane == 0) A.rowpart[i * (long long)A.stripes + stripe] = rs;
+    }
+  }
+  // column partial of this segment: fixed-order cross-warp sum
+  __syncthreads();  // red reused across segments
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) red[warp][v * 32 * VEC + lane * VEC + e] = cacc[v][e];
+  __syncthreads();
+  double* dst = A.colpart + (long long)tile * kStreamTN;
+  for (int t = threadIdx.x; t < kStreamTN; t += kThreads) {
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) sum += red[w][t];
+    dst[t] = sum;
+  }
+}
+
+// cp.async (LDGSTS) variant: every thread keeps a private D-deep queue of its
+// own 16-byte chunks (X, C of one row, plus the row's phi) in shared memory,
+// so D rows per warp are always in flight without holding them in registers.
+// Each thread reads back only what it copied itself: no barriers, only
+// cp.async.wait_group. .cg copies bypass L1 (phi changes every iteration).
+// L2 policies: the plan stream is read / written once per iteration
+// (evict_first); the row / column partials are re-read after the sweep
+// (evict_last), so they survive the 4.8 GB that streams past them.
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_hint(double* ptr, double v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(ptr), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(float4* ptr, float4 v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_hint(double2* ptr, double2 v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(ptr), "d"(v.x), "d"(v.y),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, unsigned long long pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+               "l"(gmem), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <typename T, int NV, int D>
+__host__ __device__ constexpr size_t stream_async_smem() {
+  return size_t(D) * size_t(2 * NV + 1) * kThreads * 16;
+}
+
+template <typename T, int REG, bool EXACT, int NV, int D>
+__device__ __forceinline__ void stream_segment_async(const StreamArgs& A, int tile, long long stripe,
+                                                     long long r0, long long r1, double rho,
+                                                     double qd, double qinv,
+                                                     double (*red)[kStreamTN], uint4* q) {
+  using V = typename Vec<T>::type;
+  constexpr int VEC = Vec<T>::N;
+  constexpr int NS = 2 * NV + 1;  // 16-byte slots per row: X[NV], C[NV], phi
+  static_assert(32 * VEC * NV == kStreamTN, "stripe width");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T* X = static_cast<T*>(A.X);
+  const T* C = static_cast<const T*>(A.C);
+  const long long col0 = stripe * kStreamTN;
+  long long cols[NV];
+  bool cok[NV];
+  double psi_r[NV][VEC], cacc[NV][VEC];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    cols[v] = col0 + v * 32 * VEC + lane * VEC;
+    cok[v] = cols[v] < A.ld;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      psi_r[v][e] = cok[v] ? __ldcg(A.psi + cols[v] + e) : 0.0;
+      cacc[v][e] = 0.0;
+    }
+  }
+  const unsigned long long pfirst = policy_evict_first(), plast = policy_evict_last();
+  auto slot = [&](int st, int k) -> uint4* { return q + ((size_t)(st * NS + k) * kThreads + threadIdx.x); };
+  auto issue = [&](long long i, int st) {
+    if (i < r1) {
+      const T* xrow = X + i * A.ld;
+      const T* crow = C + i * A.ld;
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        if (cok[v]) {
+          cp_async16(slot(st, v), xrow + cols[v], pfirst);
+          cp_async16(slot(st, NV + v), crow + cols[v], pfirst);
+        }
+      cp_async16(slot(st, 2 * NV), A.phi + (i & ~1LL));
+    }
+    cp_async_commit();
+  };
+  const long long step = kWarps;
+  long long i = r0 + warp;
+#pragma unroll
+  for (int d = 0; d < D - 1; ++d) issue(i + d * step, d);
+  int st = 0;
+  for (; i < r1; i += step) {
+    issue(i + (D - 1) * step, (st + D - 1) % D);
+    cp_async_wait<D - 1>();
+    const double2 ph2 = *reinterpret_cast<const double2*>(slot(st, 2 * NV));
+    const double ph = (i & 1) ? ph2.y : ph2.x;
+    double rs = 0.0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (!cok[v]) continue;
+      double x[VEC], cc[VEC], o[VEC];
+      unpack(*reinterpret_cast<const V*>(slot(st, v)), x);
+      unpack(*reinterpret_cast<const V*>(slot(st, NV + v)), cc);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, cc[e])), ph),
+                                             psi_r[v][e])
+                                 : (fma(-rho, cc[e], x[e]) + ph) + psi_r[v][e];
+        double nx = clamp0(val);
+        if (REG == REG_QUAD) nx = EXACT ? __ddiv_rn(nx, qd) : nx * qinv;
+        o[e] = nx;
+        cacc[v][e] += nx;
+        rs += nx;
+      }
+      st_hint(reinterpret_cast<V*>(X + i * A.ld) + cols[v] / VEC, pack<T>(o), pfirst);
+    }
+    rs = warp_sum(rs);
+    if (lane == 0) st_hint(A.rowpart + i * (long long)A.stripes + stripe, rs, plast);
+    st = (st + 1 == D) ? 0 : st + 1;
+  }
+  cp_async_wait<0>();  // drain the (empty) tail groups before the queue is reused
+  __syncthreads();
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) red[warp][v * 32 * VEC + lane * VEC + e] = cacc[v][e];
+  __syncthreads();
+  double* dst = A.colpart + (long long)tile * kStreamTN;
+  for (int t = threadIdx.x; t < kStreamTN; t += kThreads) {
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) sum += red[w][t];
+    st_hint(dst + t, sum, plast);
+  }
+}
+
+// The CTA that completes the last tile of a stripe folds the stripe's column
+// partials in tile order: S_j -> s_j = S_j - q_j, and the stripe's sum of
+// s_j^2 (column folds leave the critical path except for the last stripes).
+__device__ __forceinline__ void stream_stripe_done(const StreamArgs& A, long long stripe,
+                                                   double* sred, bool* s_last) {
+  __threadfence();  // this thread's colpart stores
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned need = (unsigned)(A.sfirst[stripe + 1] - A.sfirst[stripe]);
+    *s_last = atomicAdd(A.scnt + stripe, 1u) == need - 1;
+  }
+  __syncthreads();
+  if (!*s_last) return;
+  __threadfence();
+  const long long j = stripe * kStreamTN + threadIdx.x;
+  double ss = 0.0;
+  if (threadIdx.x < kStreamTN && j < A.n) {
+    const double* src = A.colpart + threadIdx.x;
+    const int t0 = A.sfirst[stripe], t1 = A.sfirst[stripe + 1];
+    double S = 0.0;
+#pragma unroll 16
+    for (int t = t0; t < t1; ++t) S += __ldcg(src + (long long)t * kStreamTN);
+    const double sj = __dsub_rn(S, A.q[j]);
+    A.s[j] = sj;
+    ss = sj * sj;
+  }
+  const double tot = block_sum(ss, sred);
+  if (threadIdx.x == 0) {
+    A.sspart[stripe] = tot;
+    A.scnt[stripe] = 0;  // every tile of this stripe is done for this iteration
+  }
+}
+
+template <typename T, int REG, bool EXACT, int NV, int U, int D>
+__global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
+  Ctl* ctl = A.ctl;
+  if (ctl->done) return;  // grid-uniform
+  const Params& prm = *A.prm;
+  // column-partial staging: aliases the (drained) cp.async queue when there is one
+  extern __shared__ __align__(16) uint4 squeue[];
+  __shared__ double red_static[D > 0 ? 1 : kWarps][kStreamTN];
+  double(*red)[kStreamTN] = D > 0 ? reinterpret_cast<double(*)[kStreamTN]>(squeue) : red_static;
+  __shared__ double sred[kWarps];
+  __shared__ double bc[4];
+  const int c = (int)blockIdx.x, P = (int)gridDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long m = A.m, n = A.n;
+  __shared__ unsigned s_tile;
+  __shared__ bool s_last;
+  const long long gwarp = (long long)c * kWarps + warp, nwarps = (long long)P * kWarps;
+  const long long gtid = (long long)c * kThreads + threadIdx.x, nthr = (long long)P * kThreads;
+
+  const double rho = prm.rho, qd = prm.quad_d, qinv = prm.quad_inv;
+  const double dm = (double)m, dn = (double)n, mn = (double)(m + n);
+  long long k = ctl->k;
+  double theta = ctl->theta[k & 1];
+  double best = ctl->best;
+  long long last_imp = ctl->last_improvement;
+  const long long k0 = ctl->k0;
+  long long it = 0;
+
+  auto stamp = [&](int slot) {
+    if (A.tstamp && it < kTraceIters && threadIdx.x == 0 && (slot < P ? true : c == 0))
+      A.tstamp[it * (P + 8) + slot] = globaltimer_ns();
+  };
+  for (;;) {
+    stamp(P + 0);
+    // ---- A. sweep tiles claimed from the iteration's tile counter
+    for (;;) {
+      if (threadIdx.x == 0) s_tile = atomicAdd(&ctl->tile_ctr, 1u);
+      __syncthreads();
+      const int tile = (int)s_tile;  // the tile sweep ends with __syncthreads
+      if (tile >= A.ntiles) break;
+      const int4 tl = A.tiles[tile];
+      if constexpr (D > 0) {
+        stream_segment_async<T, REG, EXACT, NV, D>(A, tile, tl.x, tl.y, tl.z, rho, qd, qinv, red, squeue);
+      } else {
+        stream_segment<T, REG, EXACT, NV, U>(A, tile, tl.x, tl.y, tl.z, rho, qd, qinv, red);
+      }
+      stream_stripe_done(A, tl.x, sred, &s_last);
+    }
+    stamp(c);
+    grid_barrier(&ctl->bar_str);
+    stamp(P + 1);
+
+    // ---- B. row folds (warp per row, stripe order) and column folds (CTA order)
+    double sr = 0.0, sr2 = 0.0, sR = 0.0;
+    for (long long i0 = gwarp * 4; i0 < m; i0 += nwarps * 4) {  // 4 rows per warp trip
+      double R[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int t = lane; t < A.stripes; t += 32) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i0 + u < m) R[u] += __ldcg(A.rowpart + (i0 + u) * A.stripes + t);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        R[u] = warp_sum(R[u]);
+        if (lane == 0 && i0 + u < m) {
+          const double ri = R[u] - A.p[i0 + u];
+          A.r[i0 + u] = ri;
+          sr += ri;
+          sr2 += ri * ri;
+          sR += R[u];
+        }
+      }
+    }
+    stamp(P + 5);
+    stamp(P + 6);
+    {
+      const double t1 = block_sum(sr, sred);
+      const double t2 = block_sum(sr2, sred);
+      const double t3 = block_sum(sR, sred);
+      if (threadIdx.x == 0) {
+        A.part[c * 4 + 0] = t1;
+        A.part[c * 4 + 1] = t2;
+        A.part[c * 4 + 2] = t3;
+      }
+    }
+    stamp(P + 2);
+    grid_barrier(&ctl->bar_str);
+    stamp(P + 3);
+
+    // ---- C. scalar folds (same order in every CTA), recurrence, stopping
+    if (warp < 3) {
+      double u = 0.0;
+      for (int cc = lane; cc < P; cc += 32) u += __ldcg(A.part + cc * 4 + warp);
+      u = warp_sum(u);
+      if (lane == 0) bc[warp] = u;
+    } else if (warp == 3) {  // sum s^2: stripe partials in stripe order
+      double u = 0.0;
+      for (int t = lane; t < A.stripes; t += 32) u += __ldcg(A.sspart + t);
+      u = warp_sum(u);
+      if (lane == 0) bc[3] = u;
+    }
+    __syncthreads();
+    if (c == 0 && threadIdx.x == 0) ctl->tile_ctr = 0;  // every CTA is past its last claim
+    const double eta = __ddiv_rn(bc[0], mn);
+    const double shift = __dsub_rn(2.0 * eta, theta);
+    for (long long i = gtid; i < m; i += nthr) {
+      const double ri = __ldcg(A.r + i), ai = A.a[i];
+      A.phi[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift), dn);
+      A.a[i] = __dsub_rn(ai, ri);
+    }
+    for (long long j = gtid; j < n; j += nthr) {
+      const double sj = __ldcg(A.s + j), bj = A.b[j];
+      A.psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift), dm);
+      A.b[j] = __dsub_rn(bj, sj);
+    }
+    stamp(P + 4);
+    const double nr2 = sqrt(bc[1]), ns2 = sqrt(bc[3]);
+    const double rp = (nr2 < ns2) ? ns2 : nr2;  // std::max semantics (solver.cpp:179)
+    theta = __dsub_rn(theta, eta);
+    ++k;
+    ++it;
+    const long long kk = k - k0;
+    bool done = false;
+    int term = TERM_MAXITER;
+    if (prm.solving) {
+      if (!(rp - rp == 0.0)) {  // solver.cpp:181-185
+        done = true;
+        term = TERM_NONFINITE;
+      } else {
+        if (rp < best * (1.0 - 1e-14)) {  // solver.cpp:200-203
+          best = rp;
+          last_imp = kk;
+        }
+        const bool at_check = (kk % prm.check_every) == 0;
+        if (at_check && rp <= prm.tol_primal) {
+          done = true;
+          term = TERM_CONVERGED;
+        } else if (kk - last_imp >= 10000) {  // solver.cpp:17, :232-235
+          done = true;
+          term = TERM_STALLED;
+        } else if (kk >= prm.max_iter) {
+          done = true;
+          term = TERM_MAXITER;
+        }
+      }
+    } else if (it >= A.iters) {
+      done = true;
+    }
+    if (done) {
+      if (c == 0 && threadIdx.x == 0) {
+        ctl->k = k;
+        ctl->theta[k & 1] = theta;
+        ctl->eta = eta;
+        ctl->r_primal = rp;
+        ctl->best = best;
+        ctl->last_improvement = last_imp;
+        if (prm.solving) {
+          ctl->done = 1;
+          ctl->termination = term;
+        }
+      }
+      break;
+    }
+    grid_barrier(&ctl->bar_str);  // phi / psi complete before the next sweep
+  }
+}
+
+}  // namespace otdrk

@@ -560,6 +560,7 @@ def test_tma_sweep_matches_register_sweep(ora, monkeypatch, storage):
     for mode in ("tma", "regs"):
         monkeypatch.setenv("OTDR_SWEEP", mode)
         monkeypatch.setenv("OTDR_RESIDENT", "off")
+        monkeypatch.setenv("OTDR_STREAM", "off")
         eng = otdr.Engine(m, n, storage)
         eng.set_problem(C, p, q)
         eng.set_regularizer(otdr.QuadraticReg(12.0))
@@ -569,3 +570,71 @@ def test_tma_sweep_matches_register_sweep(ora, monkeypatch, storage):
         eng.close()
     a, b = outs
     assert np.array_equal(a.X, b.X) and np.array_equal(a.phi, b.phi) and np.array_equal(a.psi, b.psi)
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (5, 3000), (33, 257), (300, 517), (1500, 1400), (2100, 700)])
+@pytest.mark.parametrize("kind,param", [("none", 0.0), ("quad", 0.7)])
+def test_stream_kernel_matches_oracle(ora, monkeypatch, m, n, kind, param):
+    """The persistent streaming solve kernel (one cooperative launch for the
+    whole solve / step run) against the oracle: fp64 iterates after k steps
+    within 1e-12, then a full solve with the same iteration count."""
+    monkeypatch.setenv("OTDR_RESIDENT", "off")
+    C, p, q, *_ = ora.gaussian_problem(m, n, 17 + m)
+    pr = ora.Problem(C, p, q)
+    oreg = oracle_reg(ora, kind, param, None, n)
+    st = ora.make_state(pr)
+    eng = otdr.Engine(m, n, "f64")
+    eng.set_problem(C, p, q)
+    eng.set_regularizer(dev_reg(kind, param, None, n))
+    eng.set_state()
+    rho = ora.default_stepsize(m, n)
+    done = 0
+    for k in (1, 7, 40):
+        for _ in range(k - done):
+            ora.step(st, pr, oreg, rho)
+        eng.step(rho, k - done)
+        done = k
+        g = eng.get_state()
+        assert g.k == st.k == k
+        assert rel(g.X, st.X) <= 1e-12, (k, rel(g.X, st.X))
+        assert rel(g.phi, st.phi) <= 1e-12 and rel(g.psi, st.psi) <= 1e-12
+        assert rel(g.a, st.a) <= 1e-12 and rel(g.b, st.b) <= 1e-12
+        assert rel(g.r, st.r) <= 1e-9 and rel(g.s, st.s) <= 1e-9
+        assert abs(g.theta - st.theta) <= 1e-12 * max(1.0, abs(st.theta))
+    o = ora.solve(pr, oreg, tol_primal=1e-6, max_iter=3000)
+    eng.set_state()
+    rep = eng.solve(otdr.SolverOptions(tol_primal=1e-6, max_iter=3000, storage="f64"))
+    assert rep.termination.name == o.termination
+    assert rep.iterations == o.iterations
+    assert abs(rep.objective - o.objective) <= 1e-9 * max(abs(o.objective), 1e-300)
+    assert abs(rep.r_primal - o.r_primal) <= 1e-6
+    eng.close()
+
+
+@pytest.mark.parametrize("storage", ["f64", "f32"])
+def test_stream_kernel_matches_graph_loop(ora, monkeypatch, storage):
+    """Streaming kernel vs the three-kernel CUDA-graph loop on a plan larger
+    than one wave: same trajectory (reduction order only)."""
+    m, n = 3000, 2600
+    C, p, q, *_ = ora.gaussian_problem(m, n, 3)
+    out = {}
+    for mode in ("on", "off"):
+        monkeypatch.setenv("OTDR_RESIDENT", "off")
+        monkeypatch.setenv("OTDR_STREAM", mode)
+        eng = otdr.Engine(m, n, storage)
+        eng.set_problem(C, p, q)
+        eng.set_regularizer(otdr.QuadraticReg(5e-3 * (m + n)))
+        eng.set_state()
+        eng.step(otdr.default_stepsize(m, n), 25)
+        st = eng.get_state()
+        eng.set_state()
+        rep = eng.solve(otdr.SolverOptions(tol_primal=1e-5, max_iter=5000, storage=storage))
+        out[mode] = (st, rep)
+        eng.close()
+    a, b = out["on"], out["off"]
+    tol = 1e-12 if storage == "f64" else 1e-6
+    assert a[0].k == b[0].k == 25
+    assert rel(a[0].X, b[0].X) <= tol and rel(a[0].phi, b[0].phi) <= tol and rel(a[0].psi, b[0].psi) <= tol
+    assert a[1].termination == b[1].termination
+    assert abs(a[1].iterations - b[1].iterations) <= (0 if storage == "f64" else 2)
+    assert abs(a[1].objective - b[1].objective) <= (1e-9 if storage == "f64" else 1e-6) * abs(b[1].objective)
