@@ -13,8 +13,12 @@ value  : DR iterations/s with C and X resident in HBM (device time, CUDA events,
 e2e    : the same metric through the public API (otdr.solve on a host fp64
          Problem in pinned memory): cost upload, the device solve, and the plan
          download are all inside the timed region.
-roofline: the sweep kernel (12 B / plan entry / iteration) against the measured
-         HBM copy bandwidth of MEASURED_PEAKS.json.
+roofline: the dominant kernel against the measured HBM copy bandwidth of
+         MEASURED_PEAKS.json, algorithmic bytes 12 B / plan entry / iteration
+         (read C, read X, write X). One GPU: the persistent streaming solve
+         kernel -- ONE launch runs all timed iterations, so bytes per launch =
+         12 m n K and its duration is the CUDA-event time of that launch.
+         Row-sharded (N > 1): the per-iteration sweep kernel.
 cpu_baseline: the CPU oracle (oracle/, a restatement of the reference solver;
          the reference itself needs Eigen, absent here) on the host cores.
 
@@ -63,14 +67,15 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the sweep from the committed ncu summary."""
-    path = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
+def ncu_traffic(kernel: str):
+    """DRAM bytes per DR iteration of `kernel` from the committed ncu summary
+    (profiles/ncu_<kernel>_summary.json, one `ncu --set full` capture)."""
+    path = os.path.join(ROOT, "profiles", f"ncu_{kernel}_summary.json")
     try:
         with open(path) as f:
             d = json.load(f)
         if d.get("workload") == WORKLOAD:
-            return d.get("dram_bytes_per_launch")
+            return d.get("dram_bytes_per_iteration")
     except Exception:
         pass
     return None
@@ -257,11 +262,28 @@ def run_ours(args):
     value = args.steps / (ms / 1e3)
     clocks = clk.summary()
 
-    # roofline: the sweep kernel timed per launch with CUDA events
+    path = eng.solve_path()
+    # component times of the graph path (sweep / reduce / all-reduce / update
+    # kernels, CUDA events per launch) -- the roofline kernel when sharded
     prof = eng.profile(rho, 10)
-    achieved = prof["sweep_bytes"] / (prof["sweep_ms"] * 1e-3) / 1e9
     peak, peak_src = measured_peak()
-    traffic = ncu_traffic()
+    if path == "stream":
+        bytes_per_launch = prof["sweep_bytes"] * args.steps
+        achieved = bytes_per_launch / (ms * 1e-3) / 1e9
+        tr = ncu_traffic("stream")
+        roof = {"kernel": "stream_kernel (persistent solve: sweep + partial folds + recurrence, "
+                          f"one launch for all {args.steps} timed iterations)",
+                "bytes_per_launch": bytes_per_launch, "launch_ms": ms,
+                "traffic": tr * args.steps if tr else None}
+    else:
+        achieved = prof["sweep_bytes"] / (prof["sweep_ms"] * 1e-3) / 1e9
+        tr = ncu_traffic("sweep")
+        roof = {"kernel": "sweep_kernel (fused clamp+prox+row/col partial sums)",
+                "bytes_per_launch": prof["sweep_bytes"], "launch_ms": prof["sweep_ms"],
+                "traffic": tr}
+    roof.update({"graph_path_sweep_ms": prof["sweep_ms"], "graph_path_reduce_ms": prof["reduce_ms"],
+                 "graph_path_exchange_ms": prof["exchange_ms"], "graph_path_update_ms": prof["update_ms"],
+                 "peak_source": peak_src})
 
     # time to tolerance (device-resident solve loop)
     t_rep = eng.solve(otdr.SolverOptions(tol_primal=1e-4, max_iter=5000, storage="f32"),
@@ -291,17 +313,14 @@ def run_ours(args):
                        "alpha": ALPHA, "rho": rho, "storage": "f32", "arithmetic": "f64",
                        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
                        "l2": "inputs (3.2 GB C+X) larger than the 126 MB L2; no flush"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "sweep (fused clamp+prox+row/col partial sums)",
-                         "bytes_per_launch": prof["sweep_bytes"], "sweep_ms": prof["sweep_ms"],
-                         "reduce_ms": prof["reduce_ms"], "exchange_ms": prof["exchange_ms"],
-                         "update_ms": prof["update_ms"], "peak_source": peak_src},
+            "roofline": dict({"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                              "frac": achieved / peak}, **roof),
             "time_to_tol": {"tol_primal": 1e-4, "iterations": t_rep.iterations,
                             "termination": t_rep.termination.name, "device_s": tt / 1e3},
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": args.steps * kpi,
+            "gpu_launches": 1 if kpi == 0 else args.steps * kpi,
+            "device_loop": path,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

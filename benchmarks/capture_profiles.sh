@@ -1,0 +1,19 @@
+#!/bin/bash
+# Round profile capture on one B200 (run under gpurun from the repo root).
+# Writes gpurun_out/: bench.log (the driver line), launches.csv (ncu launch
+# list of a short bench run), stream.ncu-rep (--set full, the timed stream
+# kernel launch of K=2 iterations), sweep.ncu-rep (graph-path sweep kernel),
+# gl.ncu-rep (cfg3 group-lasso sweep).
+set -u
+mkdir -p gpurun_out
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e \
+  > gpurun_out/launches_bench.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_kernel -s 1 -c 1 \
+  -o gpurun_out/stream -f python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_stream.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 3 -c 1 \
+  -o gpurun_out/sweep -f python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_sweep.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gl_ -s 3 -c 1 \
+  -o gpurun_out/gl -f python benchmarks/variants.py cfg3 > gpurun_out/ncu_gl.log 2>&1
+echo done

@@ -191,8 +191,14 @@ otdr_status otdr_dev_profile(otdr_dev* ctx, double rho, int64_t iters, otdr_kern
 /* Device time (CUDA events on the context stream) of `iters` graph-launched
  * raw steps; state advances by iters. */
 otdr_status otdr_dev_time_steps(otdr_dev* ctx, double rho, int64_t iters, double* ms);
-/* Number of kernel launches one DR iteration issues (sweep, reduce, update). */
+/* Number of kernel launches one DR iteration issues on the graph path
+ * (sweep, reduce, update); 0 when iterations run inside one persistent
+ * launch (on-chip resident or streaming solve kernel). */
 int otdr_dev_kernels_per_iteration(const otdr_dev* ctx);
+/* Which device loop step()/solve() use for the current configuration
+ * (no certificate / trace / fused): OTDR_PATH_* below. */
+enum { OTDR_PATH_GRAPH = 0, OTDR_PATH_RESIDENT = 1, OTDR_PATH_STREAM = 2 };
+int otdr_dev_solve_path(const otdr_dev* ctx);
 
 /* ---------------------------------------------------------------- batched
  * B independent problems of one shape solved by ONE launch, each problem owned

@@ -66,7 +66,7 @@ EXPORTS = [
     "otdr_dev_set_regularizer", "otdr_dev_set_state", "otdr_dev_load_state", "otdr_dev_step",
     "otdr_dev_solve", "otdr_dev_get_state", "otdr_dev_objective", "otdr_dev_duality_gap",
     "otdr_dev_get_trace", "otdr_dev_profile", "otdr_dev_time_steps",
-    "otdr_dev_kernels_per_iteration", "otdr_dev_read_cost_otpb", "otdr_dev_write_plan_otpb",
+    "otdr_dev_kernels_per_iteration", "otdr_dev_solve_path", "otdr_dev_read_cost_otpb", "otdr_dev_write_plan_otpb",
     "otdr_batch_create", "otdr_batch_destroy", "otdr_batch_last_error", "otdr_batch_set_problems",
     "otdr_batch_build_sqdist_costs", "otdr_batch_set_regularizer", "otdr_batch_solve",
     "otdr_batch_get_plans",
@@ -129,6 +129,8 @@ def lib():
     L.otdr_batch_get_plans.argtypes = [vp, _dp, _dp, _dp]
     L.otdr_dev_kernels_per_iteration.argtypes = [vp]
     L.otdr_dev_kernels_per_iteration.restype = ct.c_int
+    L.otdr_dev_solve_path.argtypes = [vp]
+    L.otdr_dev_solve_path.restype = ct.c_int
     _lib = L
     return L
 

@@ -1026,7 +1026,15 @@ int otdr_dev_cuda_available(void) {
 
 const char* otdr_dev_last_error(const otdr_dev* ctx) { return ctx ? ctx->err.c_str() : ""; }
 
+int otdr_dev_solve_path(const otdr_dev* ctx) {
+  if (!ctx) return OTDR_PATH_GRAPH;
+  if (ctx->resident_active(false, false)) return OTDR_PATH_RESIDENT;
+  if (ctx->stream_active(false, false)) return OTDR_PATH_STREAM;
+  return OTDR_PATH_GRAPH;
+}
+
 int otdr_dev_kernels_per_iteration(const otdr_dev* ctx) {
+  if (otdr_dev_solve_path(ctx) != OTDR_PATH_GRAPH) return 0;
   // sweep + finalize (single GPU) / sweep + reduce + update
   return (ctx && (ctx->comm || !ctx->use_fused_finalize)) ? 3 : 2;
 }

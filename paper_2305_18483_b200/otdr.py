@@ -584,7 +584,12 @@ class Engine:
         return ms.value
 
     def kernels_per_iteration(self) -> int:
+        """Launches per DR iteration on the graph path; 0 for persistent loops."""
         return self._L.otdr_dev_kernels_per_iteration(self._h)
+
+    def solve_path(self) -> str:
+        """Device loop used by step()/solve(): "graph", "resident" or "stream"."""
+        return ("graph", "resident", "stream")[self._L.otdr_dev_solve_path(self._h)]
 
 
 class BatchEngine:
