@@ -10,6 +10,7 @@
 #include "otdr_kernels.cuh"
 #include "otdr_resident.cuh"
 #include "otdr_stream.cuh"
+#include "otdr_glpipe.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -167,6 +168,9 @@ struct otdr_dev {
   int glr_g = 0, glr_groups = 0, glr_nb = 0;
   size_t glr_smem = 0;
   CUtensorMap glr_mapX{}, glr_mapC{};
+  // pipelined single-pass GL sweep: persistent CTAs over (segment, G stripes)
+  int glp_G = 0, glp_nstr = 0, glp_groups = 0, glp_lmax = 0, glp_d = 0;
+  size_t glp_smem = 0;
   // TMA-pipelined plain sweep (OTDR_SWEEP=tma): box 256 cols x kSweepTR rows
   bool use_tma_sweep = false;
   CUtensorMap sw_mapX{}, sw_mapC{};
@@ -233,7 +237,10 @@ struct otdr_dev {
 
   // The cluster kernel covers the plain (non-fused, untracked) iteration; the
   // even/odd and support-tracking variants use the two-phase kernel.
-  bool gl_ring_active(bool track) const { return glr_g > 0 && !track && !prm.fused; }
+  bool gl_pipe_active(bool track) const { return glp_G > 0 && !track && !prm.fused; }
+  bool gl_ring_active(bool track) const {
+    return !gl_pipe_active(track) && glr_g > 0 && !track && !prm.fused;
+  }
   bool gl_stage_active(bool track) const {
     return !gl_ring_active(track) && glst_g > 0 && !track && !prm.fused;
   }
@@ -241,7 +248,31 @@ struct otdr_dev {
     return !gl_stage_active(track) && glc_tn > 0 && !track && !prm.fused;
   }
 
+  template <typename T, int D>
+  void launch_gl_pipe_t() {
+    auto kern = otdrk::gl_pipe_kernel<T, sizeof(T) == 8, D>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(glp_smem)));
+    otdrk::GLPipeArgs ga{X, C, phi, psi, rowpart, colpart, d_seg, d_prm, d_ctl, m_loc, ld,
+                         num_segs, glp_nstr, glp_G, glp_groups, glp_lmax};
+    kern<<<num_sms, otdrk::kGLPThreads, glp_smem, stream>>>(ga);
+  }
+  void launch_gl_pipe() {
+    if (f64()) {
+      if (glp_d == 4) launch_gl_pipe_t<double, 4>();
+      else if (glp_d == 3) launch_gl_pipe_t<double, 3>();
+      else launch_gl_pipe_t<double, 2>();
+    } else {
+      if (glp_d == 4) launch_gl_pipe_t<float, 4>();
+      else if (glp_d == 3) launch_gl_pipe_t<float, 3>();
+      else launch_gl_pipe_t<float, 2>();
+    }
+  }
+
   void launch_sweep(bool track, bool sums_only) {
+    if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only && gl_pipe_active(track)) {
+      launch_gl_pipe();
+      return;
+    }
     if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only && gl_ring_active(track)) {
       const dim3 grid{unsigned(glr_groups), unsigned(num_segs), 1u};
       if (f64()) {
@@ -362,6 +393,7 @@ struct otdr_dev {
   // by the sweep variant that runs in this configuration.
   std::pair<int, int> partial_shape(bool sums_only, bool track) const {
     if (gl_active(sums_only)) {
+      if (gl_pipe_active(track)) return {glp_groups, num_segs};
       if (gl_ring_active(track)) return {glr_groups, num_segs};
       if (gl_stage_active(track)) return {glst_groups, num_segs};
       if (gl_cluster_active(track)) return {gl_stripes, num_segs * glc_k};
@@ -715,10 +747,42 @@ struct otdr_dev {
     glr_groups = 0;
     glr_nb = 0;
     glr_smem = 0;
+    glp_G = 0;
+    glp_groups = 0;
+    glp_smem = 0;
     if (reg_kind != OTDR_REG_GROUP_LASSO || m_loc == 0) return;
     long long lmax = 0;
     for (const Segment& sg : segs) lmax = std::max(lmax, sg.end - sg.begin);
     if (lmax == 0) return;
+    {  // pipelined kernel (default): deepest cp.async queue whose staging fits
+      const char* gk0 = std::getenv("OTDR_GL_KERNEL");
+      if (!gk0 || std::strcmp(gk0, "pipe") == 0) {
+        int max_smem = 0;
+        CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg.device));
+        for (int d : {4, 3, 2}) {
+          const size_t need = f64() ? otdrk::glpipe_smem_bytes<double, 4>(int(lmax)) -
+                                          otdrk::glpipe_queue_bytes<double, 4>() +
+                                          size_t(d) * 2 * otdrk::kGLPThreads * 16
+                                    : otdrk::glpipe_smem_bytes<float, 4>(int(lmax)) -
+                                          otdrk::glpipe_queue_bytes<float, 4>() +
+                                          size_t(d) * 2 * otdrk::kGLPThreads * 16;
+          if (need + 1024 <= size_t(max_smem)) {
+            glp_d = d;
+            glp_smem = need;
+            break;
+          }
+        }
+        if (glp_smem) {
+          const long long W = 128 / (long long)esz;
+          glp_nstr = int((ld + W - 1) / W);
+          glp_G = 8;
+          if (const char* ge = std::getenv("OTDR_GL_PIPE_G"))
+            glp_G = std::max(1, std::min(otdrk::kGLPMaxG, std::atoi(ge)));
+          glp_groups = (glp_nstr + glp_G - 1) / glp_G;
+          glp_lmax = int(lmax);
+        }
+      }
+    }
     // segment-staged kernel: the whole segment's v for a 64-byte stripe in
     // shared memory (<= 100 KB: two or three CTAs per SM); OTDR_GL_KERNEL
     // selects stage / cluster / twopass explicitly.
@@ -780,7 +844,7 @@ struct otdr_dev {
 
   void ensure_partials() {
     const int seg_stripes = int((ld + tn_seg() - 1) / tn_seg());
-    const size_t need_row = size_t(std::max(std::max(std::max(stripes, gl_stripes), std::max(seg_stripes, glst_groups)), glr_groups)) *
+    const size_t need_row = size_t(std::max(std::max(std::max(stripes, gl_stripes), std::max(seg_stripes, glst_groups)), std::max(glr_groups, glp_groups))) *
                             size_t(std::max<long long>(m_loc, 1));
     const size_t need_col = size_t(std::max(rowgroups, num_segs * std::max(glc_k, 1))) * size_t(ld);
     const size_t need_c = size_t(cert_stripes) * size_t(num_cert_segs) * otdrk::kCertVals;
@@ -1062,7 +1126,16 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     ctx->row0 = cfg->row_begin;
     ctx->m_loc = cfg->row_end - cfg->row_begin;
     const long long vec = ctx->f64() ? 2 : 4;
-    ctx->ld = (ctx->n + vec - 1) / vec * vec;
+    // rows start on 256-byte boundaries for n >= 1024. Measured on B200: a
+    // 40000-byte fp32 row pitch (n = 10000) left every other row's 128-byte
+    // chunks straddling two L2 lines (+16 % DRAM reads in the group-lasso
+    // sweep); 256-byte pitches stream faster than 128-byte ones (20000^2
+    // stream kernel 5.89 -> 6.04 TB/s, 10000^2 5.24 -> 5.39 TB/s).
+    long long align = vec;
+    if (ctx->n >= 1024) align = 256 / (long long)ctx->esz;
+    if (const char* la = std::getenv("OTDR_LD_ALIGN"))
+      align = std::max<long long>(vec, std::atoll(la) / (long long)ctx->esz);
+    ctx->ld = (ctx->n + align - 1) / align * align;
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&ctx->ev0));
     CK(cudaEventCreate(&ctx->ev1));

@@ -80,6 +80,8 @@ struct Ctl {
   unsigned long long bar_res;  // resident solve kernel
   unsigned long long bar_str;  // streaming solve kernel
   unsigned int tile_ctr;       // streaming kernel: tiles claimed this sweep
+  unsigned int gl_ctr;         // pipelined group-lasso sweep: items claimed
+  unsigned int gl_done;        //   CTAs finished (the last one resets both)
   unsigned int pad_;
 };
 

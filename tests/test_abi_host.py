@@ -116,3 +116,22 @@ def test_otpb_host_roundtrip(tmp_path):
     open(path, "r+b").write(b"XXXX")
     with pytest.raises(otdr.InvalidArgument):
         io.read_matrix_otpb(path)
+
+
+def test_sass_memory_descriptors_are_even_register_pairs():
+    """Every global access in the built kernels addresses its 64-bit memory
+    descriptor through an even uniform-register pair. ptxas 12.9 once emitted
+    desc[UR1] for a cp.async with an L2 cache-policy operand, which faults as
+    an illegal instruction on B200; this guards the build against that."""
+    import re
+    import shutil
+    import subprocess
+
+    lib = os.path.join(ROOT, "paper_2305_18483_b200", "libotdr_dev.so")
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(lib) or not os.path.exists(tool):
+        pytest.skip("library or cuobjdump missing")
+    sass = subprocess.run([tool, "-sass", lib], capture_output=True, text=True).stdout
+    regs = {int(r) for r in re.findall(r"desc\[UR(\d+)\]", sass)}
+    assert regs, "no SASS found"
+    assert all(r % 2 == 0 for r in regs), sorted(regs)

@@ -371,7 +371,7 @@ def test_large_fp32_properties(ora):
     np.testing.assert_allclose(g.X.sum(axis=1) - p, g.r, atol=1e-9)
 
 
-@pytest.mark.parametrize("kernel", ["auto", "ring", "stage", "cluster", "twopass"])
+@pytest.mark.parametrize("kernel", ["auto", "pipe", "ring", "stage", "cluster", "twopass"])
 @pytest.mark.parametrize("storage,m,n,classes", [
     ("f64", 3000, 300, 2),    # long segments: cluster of 8 CTAs (DSMEM norms)
     ("f32", 3000, 301, 2),
