@@ -115,7 +115,9 @@ def run_batched(cfg, B, m, storage, tol=1e-4):
     reps = be.solve(opt)
     wall = time.perf_counter() - t0
     total = sum(r.iterations for r in reps)
-    line(cfg, B=B, m=m, n=m, storage=storage, mode="batched cluster-resident (one launch)",
+    line(cfg, B=B, m=m, n=m, storage=storage, mode=("batched cluster-resident (one launch)"
+                                                     if os.environ.get("OTDR_BATCH") == "resident"
+                                                     else "batched CTA-per-problem streaming (one launch)"),
          total_iterations=total, wall_s=wall, device_s=reps[0].device_ms / 1e3,
          problem_iters_per_s=total / (reps[0].device_ms / 1e3), mean_iters=total / B,
          max_iters=max(r.iterations for r in reps),
@@ -170,6 +172,10 @@ def main():
                       fused=a.fused, max_iter=3000)
         elif c == "cfg5":
             run_batched("cfg5", 256, 512, "f32")
+        elif c == "cfg5-resident":
+            os.environ["OTDR_BATCH"] = "resident"
+            run_batched("cfg5", 256, 512, "f32")
+            os.environ.pop("OTDR_BATCH")
         elif c == "cfg5-seq":
             run_batched_sequential("cfg5", 256, 512, "f32")
         elif c == "headline":

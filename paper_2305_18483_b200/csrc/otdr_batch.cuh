@@ -38,6 +38,12 @@ struct otdr_batch {
   long long B = 0, m = 0, n = 0, ld = 0;
   int G = 0, R = 0;
   size_t smem = 0;
+  // streaming mode: one CTA per problem, C / X streamed from HBM every iteration
+  bool use_stream = false;
+  int bs_nch = 0, bs_nsets = 0;
+  size_t bs_smem = 0;
+  static constexpr int kBSD = 3;
+  int bs_nt = 512;  // threads per problem CTA (OTDR_BATCH_THREADS=256: two CTAs per SM)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::string err;
@@ -72,8 +78,27 @@ struct otdr_batch {
     BCK(cudaMemcpy(C, buf.data(), buf.size() * sizeof(T), cudaMemcpyHostToDevice));
   }
 
+  template <typename T, int NT>
+  void launch_stream_nt() {
+    auto kern = otdrk::bstream_kernel<T, sizeof(T) == 8, kBSD, NT>;
+    BCK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bs_smem)));
+    otdrk::BStreamArgs ba{X, C, m * ld, phi, a, r, p, psi, b, s, q, ctl, prm, m, n, ld,
+                          bs_nch, bs_nsets, reg == OTDR_REG_QUAD ? otdrk::REG_QUAD : otdrk::REG_NONE};
+    kern<<<unsigned(B), NT, bs_smem, stream>>>(ba);
+    BCK(cudaGetLastError());
+  }
+  template <typename T>
+  void launch_stream() {
+    if (bs_nt == 512) launch_stream_nt<T, 512>();
+    else launch_stream_nt<T, 256>();
+  }
+
   template <typename T>
   void launch() {
+    if (use_stream) {
+      launch_stream<T>();
+      return;
+    }
     auto kern = otdrk::resident_kernel<T, true>;
     BCK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     if (G > 8) BCK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -150,7 +175,22 @@ otdr_status otdr_batch_create(int device, otdr_storage storage, int64_t batch, i
         break;
       }
     }
-    if (bt->G == 0) {
+    {  // streaming mode (default when it fits): one CTA per problem
+      const long long vecw = 32 * (bt->f64() ? 2 : 4);
+      const long long nch = (bt->ld + vecw - 1) / vecw;
+      if (const char* bn = std::getenv("OTDR_BATCH_THREADS")) bt->bs_nt = std::atoi(bn) == 256 ? 256 : 512;
+      const int nw = bt->bs_nt / 32;
+      if (nch <= nw) {
+        bt->bs_nch = int(nch);
+        bt->bs_nsets = int(nw / nch);
+        bt->bs_smem = bt->bs_nt == 512
+                          ? otdrk::bstream_smem_bytes<double, otdr_batch::kBSD, 512>(m, bt->ld, bt->bs_nch, bt->bs_nsets)
+                          : otdrk::bstream_smem_bytes<double, otdr_batch::kBSD, 256>(m, bt->ld, bt->bs_nch, bt->bs_nsets);
+        const char* bm = std::getenv("OTDR_BATCH");
+        bt->use_stream = bt->bs_smem + 1024 <= size_t(max_smem) && !(bm && std::strcmp(bm, "resident") == 0);
+      }
+    }
+    if (bt->G == 0 && !bt->use_stream) {
       delete bt;
       return OTDR_E_UNSUPPORTED;
     }

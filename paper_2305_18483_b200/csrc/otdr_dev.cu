@@ -11,6 +11,7 @@
 #include "otdr_resident.cuh"
 #include "otdr_stream.cuh"
 #include "otdr_glpipe.cuh"
+#include "otdr_bstream.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -170,6 +171,7 @@ struct otdr_dev {
   CUtensorMap glr_mapX{}, glr_mapC{};
   // pipelined single-pass GL sweep: persistent CTAs over (segment, G stripes)
   int glp_G = 0, glp_nstr = 0, glp_groups = 0, glp_lmax = 0, glp_d = 0;
+  int2* d_glp_pos = nullptr;
   size_t glp_smem = 0;
   // TMA-pipelined plain sweep (OTDR_SWEEP=tma): box 256 cols x kSweepTR rows
   bool use_tma_sweep = false;
@@ -252,8 +254,8 @@ struct otdr_dev {
   void launch_gl_pipe_t() {
     auto kern = otdrk::gl_pipe_kernel<T, sizeof(T) == 8, D>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(glp_smem)));
-    otdrk::GLPipeArgs ga{X, C, phi, psi, rowpart, colpart, d_seg, d_prm, d_ctl, m_loc, ld,
-                         num_segs, glp_nstr, glp_G, glp_groups, glp_lmax};
+    otdrk::GLPipeArgs ga{X, C, phi, psi, rowpart, colpart, d_seg, d_glp_pos, d_prm, d_ctl, m_loc, ld,
+                         num_segs, glp_nstr, glp_groups, glp_lmax};
     kern<<<num_sms, otdrk::kGLPThreads, glp_smem, stream>>>(ga);
   }
   void launch_gl_pipe() {
@@ -778,7 +780,20 @@ struct otdr_dev {
           glp_G = 8;
           if (const char* ge = std::getenv("OTDR_GL_PIPE_G"))
             glp_G = std::max(1, std::min(otdrk::kGLPMaxG, std::atoi(ge)));
-          glp_groups = (glp_nstr + glp_G - 1) / glp_G;
+          // stripe positions: runs of glp_G stripes, then runs of 2 for the
+          // last ~2 items per CTA (claimed last, position-major)
+          const long long tail_items = 2LL * num_sms;
+          long long tail_str = std::min<long long>(glp_nstr, 2 * ((tail_items + num_segs - 1) / num_segs));
+          std::vector<int2> pos;
+          const long long head = glp_nstr - tail_str;
+          for (long long s0 = 0; s0 < head; s0 += glp_G)
+            pos.push_back(int2{int(s0), int(std::min<long long>(glp_G, head - s0))});
+          for (long long s0 = head; s0 < glp_nstr; s0 += 2)
+            pos.push_back(int2{int(s0), int(std::min<long long>(2, glp_nstr - s0))});
+          glp_groups = int(pos.size());
+          if (d_glp_pos) cudaFree(d_glp_pos);
+          d_glp_pos = dalloc<int2>(pos.size());
+          CK(cudaMemcpy(d_glp_pos, pos.data(), pos.size() * sizeof(int2), cudaMemcpyHostToDevice));
           glp_lmax = int(lmax);
         }
       }
@@ -1037,7 +1052,7 @@ struct otdr_dev {
   void release() {
     invalidate_graphs();
     void* ptrs[] = {C, X, p, q, phi, psi, a, b, r, s, rowpart, colpart, exch, bpart, cpart,
-                    str_part, str_colpart, d_tiles, d_sfirst, d_scnt, str_sspart,
+                    str_part, str_colpart, d_tiles, d_sfirst, d_scnt, str_sspart, d_glp_pos,
                     csum, stage, fpart, fpart2, gscratch, d_dev_row, d_seg, d_cert_seg, d_prm, d_ctl, d_trace, d_mx};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);

@@ -9,7 +9,9 @@
 // 125 KB for a 1000-row class in fp32).
 //
 // One persistent CTA per SM (512 threads) claims work items -- (segment,
-// group of G consecutive stripes) -- from an atomic counter. Inside an item
+// position = run of up to 8 consecutive stripes) -- from an atomic counter,
+// position-major, so the short positions at the end of the stripe range
+// (2 stripes) are the last claims and CTA finish times stay close. Inside an item
 // the stripes are pipelined row by row through the SAME staging buffer:
 //   step j: for every row r of the segment
 //             phase 2 of stripe j-1: read v[r], scale by sigma_{j-1}, store X,
@@ -44,10 +46,11 @@ struct GLPipeArgs {
   double* rowpart;        // [m][ngroups]
   double* colpart;        // [nseg][ld]
   const Segment* seg;
+  const int2* pos;        // [ngroups] stripe positions {first stripe, stripes}, shared by all segments
   const Params* prm;
   Ctl* ctl;
   long long m, ld;
-  int nseg, nstr, G, ngroups, Lmax;
+  int nseg, nstr, ngroups, Lmax;
 };
 
 template <typename T, int D>
@@ -97,11 +100,12 @@ __global__ void __launch_bounds__(kGLPThreads, 1) gl_pipe_kernel(GLPipeArgs A) {
     __syncthreads();
     const int item = (int)s_item;
     if (item >= nitems) break;
-    const int si = item / A.ngroups, gi = item % A.ngroups;
+    // position-major numbering: the short tail positions are claimed last
+    const int gi = item / A.nseg, si = item % A.nseg;
     const Segment sg = A.seg[si];
     const int L = (int)(sg.end - sg.begin);
-    const int s0 = gi * A.G;
-    const int Gi = (s0 + A.G <= A.nstr) ? A.G : A.nstr - s0;
+    const int2 ps2 = A.pos[gi];
+    const int s0 = ps2.x, Gi = ps2.y;
     const int nk = (L + RSTEP - 1) / RSTEP;
     for (int t = threadIdx.x; t < L; t += kGLPThreads) {
       phi_s[t] = __ldcg(A.phi + sg.begin + t);

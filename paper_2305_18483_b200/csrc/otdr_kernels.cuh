@@ -138,6 +138,20 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return t;
 }
 
+// block_sum for NW warps (result valid in thread 0).
+template <int NW>
+__device__ __forceinline__ double block_sum_n(double v, double* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NW; ++i) t += red[i];
+  return t;
+}
+
 // Reduce-scatter of 8 row partials across a warp: lane l ends with the full
 // sum of row row8_of(l) (lanes with equal bits 2..4 share a row). 9 double
 // shuffles per 8 rows instead of 5 per row; the summation tree is fixed.

@@ -449,9 +449,12 @@ def test_resident_matches_streaming(ora, monkeypatch, storage, m, n, kind):
     assert abs(a[1].objective - b[1].objective) <= (1e-9 if storage == "f64" else 1e-6) * abs(b[1].objective)
 
 
+@pytest.mark.parametrize("mode", ["stream", "resident"])
 @pytest.mark.parametrize("storage", ["f64", "f32"])
-def test_batched_solve_matches_sequential(ora, storage):
-    """cfg5 shape at reduced batch: one cluster-resident launch == B solve()s."""
+def test_batched_solve_matches_sequential(ora, monkeypatch, storage, mode):
+    """cfg5 shape at reduced batch: one launch (CTA-per-problem streaming, or
+    cluster-resident) == B solve()s."""
+    monkeypatch.setenv("OTDR_BATCH", mode)
     B, m = 6, 96
     probs = [ora.gaussian_problem(m, m, b) for b in range(B)]
     alpha = 5e-3 * 2 * m
@@ -466,8 +469,10 @@ def test_batched_solve_matches_sequential(ora, storage):
         assert rel(rep.plan(), o.state.X) <= (1e-7 if storage == "f64" else 1e-4)
 
 
-def test_batched_device_cost_and_512(ora):
+@pytest.mark.parametrize("mode", ["stream", "resident"])
+def test_batched_device_cost_and_512(ora, monkeypatch, mode):
     """512 x 512 per problem (the cfg5 tile): device-built costs, B = 3."""
+    monkeypatch.setenv("OTDR_BATCH", mode)
     B, m = 3, 512
     src = np.empty((B, m, 2))
     tgt = np.empty((B, m, 2))
