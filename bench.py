@@ -6,7 +6,11 @@ Workload (BASELINE.json north star, SURVEY §8(d) "headline n = 20000"):
     rho = 2/(m+n), fp32 storage of C and X in HBM, fp64 arithmetic in registers.
     One "step" = one full DR iteration over the 20000 x 20000 plan.
     N > 1: the plan is row-sharded across N GPUs (one process per GPU) with one
-    NCCL all-reduce of the n+3 exchange vector per iteration -> strong scaling.
+    exchange of the n+3 vector [column sums | sum r | sum r^2 | sum X] per
+    iteration -> strong scaling. The exchange runs inside the streaming kernel
+    over NVLink peer memory (CUDA IPC; each stripe's column sums are stored to
+    every rank as soon as the stripe is swept); OTDR_PEERS=0 falls back to one
+    ncclAllReduce per iteration between kernels.
 
 value  : DR iterations/s with C and X resident in HBM (device time, CUDA events,
          max over ranks). Inputs (3.2 GB) exceed the 126 MB L2, so no flush.
@@ -166,6 +170,16 @@ def bcast_nccl_id(dist, rank):
     return sharding.broadcast_nccl_id(dist, rank)
 
 
+def connect(dist, eng, world):
+    """Row-sharded runs: link the ranks' receive buffers (CUDA IPC over
+    NVLink) so the per-iteration exchange runs inside the streaming kernel;
+    OTDR_PEERS=0 keeps the NCCL all-reduce between kernels."""
+    if world > 1 and os.environ.get("OTDR_PEERS", "1") != "0":
+        from paper_2305_18483_b200 import sharding
+
+        sharding.connect_peers(dist, eng)
+
+
 def make_engine(rank, world, dist, local_rank):
     import paper_2305_18483_b200 as otdr
     from paper_2305_18483_b200 import datagen
@@ -175,6 +189,7 @@ def make_engine(rank, world, dist, local_rank):
     if world > 1:
         shard = otdr.Shard(rank, world, lo, hi, bcast_nccl_id(dist, rank))
     eng = otdr.Engine(M, N, "f32", device=local_rank if world > 1 else 0, shard=shard)
+    connect(dist, eng, world)
     src, tgt = datagen.gaussian_points(M, N, SEED)
     eng.build_sqdist_cost(src[lo:hi], tgt, datagen.uniform(M)[lo:hi], datagen.uniform(N))
     eng.set_regularizer(otdr.QuadraticReg(ALPHA))
@@ -357,6 +372,7 @@ def e2e_measure(rank, world, dist, local_rank, args):
     plan_host = torch.empty((hi - lo, N), dtype=torch.float64, pin_memory=pin).numpy()
     shard = otdr.Shard(rank, world, lo, hi, bcast_nccl_id(dist, rank)) if world > 1 else None
     eng = otdr.Engine(M, N, "f32", device=local_rank if world > 1 else 0, shard=shard)
+    connect(dist, eng, world)
     reg = otdr.QuadraticReg(ALPHA)
     iters = args.e2e_iters
     opts = otdr.SolverOptions(tol_primal=1e-300, max_iter=iters, storage="f32")

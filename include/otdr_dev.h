@@ -85,8 +85,9 @@ typedef struct {
    * residual scalars are ncclAllReduce'd once per iteration. */
   int rank, nranks;
   int64_t row_begin, row_end;
-  const unsigned char* nccl_id; /* 128-byte ncclUniqueId; required when nranks > 1, optional
-                                  for nranks == 1 (runs the NCCL exchange path on one GPU) */
+  const unsigned char* nccl_id; /* 128-byte ncclUniqueId, or NULL. nranks > 1 needs an NCCL id
+                                  or a peer link (otdr_dev_peer_*) before the first exchange;
+                                  for nranks == 1 it runs the NCCL exchange path on one GPU */
 } otdr_dev_config;
 
 typedef struct {
@@ -191,6 +192,22 @@ otdr_status otdr_dev_profile(otdr_dev* ctx, double rho, int64_t iters, otdr_kern
 /* Device time (CUDA events on the context stream) of `iters` graph-launched
  * raw steps; state advances by iters. */
 otdr_status otdr_dev_time_steps(otdr_dev* ctx, double rho, int64_t iters, double* ms);
+/* ---------------------------------------------------------------- peers
+ * Peer-memory exchange of row-sharded runs: every rank exports a CUDA IPC
+ * handle of its receive buffer, the handles are all-gathered by the caller
+ * (any transport: torch.distributed, MPI, a file), and every rank imports all
+ * of them. From then on the solve loop's per-iteration exchange runs inside
+ * the streaming kernel over NVLink P2P stores (column sums as soon as each
+ * stripe of the sweep is complete; epoch flags at system scope) instead of an
+ * ncclAllReduce between kernels. Replaces the reference's single-process
+ * loop (solver.cpp:104-241); there is no reference counterpart to bind. */
+#define OTDR_PEER_HANDLE_BYTES 64
+otdr_status otdr_dev_peer_export(otdr_dev* ctx, void* handle /* OTDR_PEER_HANDLE_BYTES */);
+otdr_status otdr_dev_peer_import(otdr_dev* ctx, const void* handles /* nranks x 64, rank order */);
+/* Same, for the ranks of one process (contexts ctxs[r] = rank r); used to
+ * test the multi-rank path with several contexts on one GPU. */
+otdr_status otdr_dev_peer_link_local(otdr_dev** ctxs, int nranks);
+
 /* Number of kernel launches one DR iteration issues on the graph path
  * (sweep, reduce, update); 0 when iterations run inside one persistent
  * launch (on-chip resident or streaming solve kernel). */

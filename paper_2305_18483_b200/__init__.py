@@ -9,7 +9,7 @@ from .otdr import (  # noqa: F401
     InvalidArgument, MarginalSumOutOfRange, NegativeEntry, NonFiniteIterate, OtdrError, Problem,
     QuadraticReg, Regularizer, Shard, SolveReport, SolverOptions, SolverState, Termination,
     TraceRow, Unsupported, WarmStart, ZeroIterations, ZeroReg, column_class_blocks,
-    compute_skip_count, default_init, default_stepsize, duality_gap, make_partition, make_state,
+    compute_skip_count, default_init, default_stepsize, duality_gap, link_local, make_partition, make_state,
     normalize_cost, ot_cost_gradient, primal_objective, recover_duals, solve, solve_batch, step,
     to_string,
     validate_problem,

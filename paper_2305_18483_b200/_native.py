@@ -59,6 +59,8 @@ class KernelTimes(ct.Structure):
                 ("update_ms", ct.c_double), ("iterations", ct.c_int64), ("sweep_bytes", ct.c_double)]
 
 
+PEER_HANDLE_BYTES = 64  # OTDR_PEER_HANDLE_BYTES
+
 # Every symbol include/otdr_dev.h declares (checked by the CPU ABI test).
 EXPORTS = [
     "otdr_dev_abi_version", "otdr_dev_create", "otdr_dev_destroy", "otdr_dev_last_error",
@@ -66,7 +68,8 @@ EXPORTS = [
     "otdr_dev_set_regularizer", "otdr_dev_set_state", "otdr_dev_load_state", "otdr_dev_step",
     "otdr_dev_solve", "otdr_dev_get_state", "otdr_dev_objective", "otdr_dev_duality_gap",
     "otdr_dev_get_trace", "otdr_dev_profile", "otdr_dev_time_steps",
-    "otdr_dev_kernels_per_iteration", "otdr_dev_solve_path", "otdr_dev_read_cost_otpb", "otdr_dev_write_plan_otpb",
+    "otdr_dev_kernels_per_iteration", "otdr_dev_solve_path", "otdr_dev_peer_export",
+    "otdr_dev_peer_import", "otdr_dev_peer_link_local", "otdr_dev_read_cost_otpb", "otdr_dev_write_plan_otpb",
     "otdr_batch_create", "otdr_batch_destroy", "otdr_batch_last_error", "otdr_batch_set_problems",
     "otdr_batch_build_sqdist_costs", "otdr_batch_set_regularizer", "otdr_batch_solve",
     "otdr_batch_get_plans",
@@ -131,6 +134,12 @@ def lib():
     L.otdr_dev_kernels_per_iteration.restype = ct.c_int
     L.otdr_dev_solve_path.argtypes = [vp]
     L.otdr_dev_solve_path.restype = ct.c_int
+    L.otdr_dev_peer_export.argtypes = [vp, ct.c_char_p]
+    L.otdr_dev_peer_export.restype = ct.c_int
+    L.otdr_dev_peer_import.argtypes = [vp, ct.c_char_p]
+    L.otdr_dev_peer_import.restype = ct.c_int
+    L.otdr_dev_peer_link_local.argtypes = [ct.POINTER(vp), ct.c_int]
+    L.otdr_dev_peer_link_local.restype = ct.c_int
     _lib = L
     return L
 

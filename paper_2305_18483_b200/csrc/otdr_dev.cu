@@ -129,6 +129,12 @@ struct otdr_dev {
   int res_G = 0, res_R = 0;
   size_t res_smem = 0;
   double* gscratch = nullptr;
+  // peer-memory exchange of row-sharded runs (CUDA IPC over NVLink)
+  bool p2p = false;
+  double* rbuf = nullptr;            // this rank's receive buffer
+  double** d_peers = nullptr;        // [nranks] receive buffers of every rank
+  unsigned long long* d_xep = nullptr;
+  std::vector<void*> ipc_opened;
   // persistent streaming solve (single GPU, zero / quadratic, HBM-resident plan)
   bool allow_stream = true;
   int str_P = 0, str_ntiles = 0, str_tpc = 8, str_tail = 2;
@@ -412,7 +418,32 @@ struct otdr_dev {
   }
 
   void launch_exchange(double* buf, size_t count) {
-    if (comm) NK(nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, comm, stream));
+    if (comm) {
+      NK(nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, comm, stream));
+    } else if (p2p) {
+      otdrk::p2p_allreduce_kernel<<<1, 1024, 0, stream>>>(buf, (long long)count, d_peers, rbuf, d_xep,
+                                                          cfg.rank, cfg.nranks, n);
+    } else if (cfg.nranks > 1) {
+      throw Error{OTDR_E_STATE, "row-sharded context has no exchange: pass an NCCL id or link peers"};
+    }
+  }
+
+  size_t rbuf_bytes() const {
+    return size_t(2 * cfg.nranks) * size_t(n + 4) * 8 + size_t(2 * cfg.nranks) * 8;
+  }
+  void alloc_rbuf() {
+    if (rbuf) return;
+    CK(cudaMalloc(&rbuf, rbuf_bytes()));
+    CK(cudaMemset(rbuf, 0, rbuf_bytes()));
+    d_xep = dalloc<unsigned long long>(1);
+    CK(cudaMemset(d_xep, 0, 8));
+  }
+  void set_peers(const std::vector<double*>& peers) {
+    if (!d_peers) d_peers = dalloc<double*>(size_t(cfg.nranks));
+    CK(cudaMemcpy(d_peers, peers.data(), size_t(cfg.nranks) * sizeof(double*), cudaMemcpyHostToDevice));
+    p2p = true;
+    invalidate_graphs();
+    plan_stream();
   }
 
   void launch_update(cudaGraphConditionalHandle cond, int use_cond, int cert_follows) {
@@ -564,13 +595,16 @@ struct otdr_dev {
   // the plain sweep's geometry (rows_per_cta x 256 columns).
   void plan_stream() {
     str_P = 0;
-    if (!allow_stream || sharded || m_loc < 1 || reg_kind == OTDR_REG_GROUP_LASSO) return;
+    if (!allow_stream || (sharded && !p2p) || m_loc < 1 || reg_kind == OTDR_REG_GROUP_LASSO) return;
     int occ = 0;
     if (str_d < 0) str_d = default_stream_d();
     cudaLaunchConfig_t lc{};
     stream_dispatch(lc, otdrk::StreamArgs{}, &occ);
     if (occ < 1) return;
-    const long long P = (long long)num_sms * occ;
+    long long P = (long long)num_sms * occ;
+    // OTDR_STREAM_GRID caps the persistent grid (several ranks' kernels
+    // sharing one GPU in the multi-context tests must all be co-resident)
+    if (const char* sg = std::getenv("OTDR_STREAM_GRID")) P = std::max(1LL, std::min(P, std::atoll(sg)));
     const long long S = (ld + otdrk::kStreamTN - 1) / otdrk::kStreamTN;
     // long tiles (the plain sweep's rows_per_cta), short ones for the last
     // stripes, about two rounds of long tiles' worth of rows
@@ -654,7 +688,8 @@ struct otdr_dev {
     const long long S = (ld + otdrk::kStreamTN - 1) / otdrk::kStreamTN;
     otdrk::StreamArgs sa{X, C, phi, a, r, p, psi, b, s, q, rowpart, str_colpart, d_tiles,
                          d_sfirst, d_scnt, str_sspart, str_part, d_ctl, d_prm, m_loc, n, ld, int(S), str_ntiles,
-                         iters, nullptr};
+                         iters, nullptr, m_glob, sharded ? d_peers : nullptr, rbuf, d_xep,
+                         cfg.rank, cfg.nranks};
     static const bool trace = std::getenv("OTDR_STREAM_TRACE") != nullptr;
     unsigned long long* ts = nullptr;
     const size_t tsn = size_t(otdrk::kTraceIters) * size_t(str_P + 8);
@@ -1061,6 +1096,10 @@ struct otdr_dev {
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
     if (comm && nccl().ok) nccl().CommDestroy(comm);
+    for (void* ptr : ipc_opened) cudaIpcCloseMemHandle(ptr);
+    if (rbuf) cudaFree(rbuf);
+    if (d_peers) cudaFree(d_peers);
+    if (d_xep) cudaFree(d_xep);
   }
 };
 
@@ -1112,6 +1151,68 @@ int otdr_dev_solve_path(const otdr_dev* ctx) {
   return OTDR_PATH_GRAPH;
 }
 
+otdr_status otdr_dev_peer_export(otdr_dev* ctx, void* handle) {
+  if (!ctx || !handle) return OTDR_E_INVALID_ARG;
+  return guarded(ctx, [&] {
+    ctx->alloc_rbuf();
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, ctx->rbuf));
+    std::memcpy(handle, &h, sizeof(h));
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_peer_import(otdr_dev* ctx, const void* handles) {
+  if (!ctx || !handles) return OTDR_E_INVALID_ARG;
+  if (!ctx->sharded) return fail(ctx, OTDR_E_STATE, "peer exchange needs a row-sharded context");
+  return guarded(ctx, [&] {
+    ctx->alloc_rbuf();
+    const int nr = ctx->cfg.nranks;
+    std::vector<double*> peers(static_cast<size_t>(nr), nullptr);
+    for (int r = 0; r < nr; ++r) {
+      if (r == ctx->cfg.rank) {
+        peers[size_t(r)] = ctx->rbuf;
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const unsigned char*>(handles) + size_t(r) * OTDR_PEER_HANDLE_BYTES,
+                  sizeof(h));
+      void* ptr = nullptr;
+      CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+      ctx->ipc_opened.push_back(ptr);
+      peers[size_t(r)] = static_cast<double*>(ptr);
+    }
+    ctx->set_peers(peers);
+    return OTDR_OK;
+  });
+}
+
+otdr_status otdr_dev_peer_link_local(otdr_dev** ctxs, int nranks) {
+  if (!ctxs || nranks < 1) return OTDR_E_INVALID_ARG;
+  for (int r = 0; r < nranks; ++r) {
+    if (!ctxs[r]) return OTDR_E_INVALID_ARG;
+    if (ctxs[r]->cfg.nranks != nranks || ctxs[r]->cfg.rank != r || !ctxs[r]->sharded)
+      return fail(ctxs[r], OTDR_E_STATE, "contexts must be the ranks 0..nranks-1 of one sharded run");
+  }
+  std::vector<double*> peers(static_cast<size_t>(nranks), nullptr);
+  for (int r = 0; r < nranks; ++r) {
+    const otdr_status st = guarded(ctxs[r], [&] {
+      ctxs[r]->alloc_rbuf();
+      peers[size_t(r)] = ctxs[r]->rbuf;
+      return OTDR_OK;
+    });
+    if (st != OTDR_OK) return st;
+  }
+  for (int r = 0; r < nranks; ++r) {
+    const otdr_status st = guarded(ctxs[r], [&] {
+      ctxs[r]->set_peers(peers);
+      return OTDR_OK;
+    });
+    if (st != OTDR_OK) return st;
+  }
+  return OTDR_OK;
+}
+
 int otdr_dev_kernels_per_iteration(const otdr_dev* ctx) {
   if (otdr_dev_solve_path(ctx) != OTDR_PATH_GRAPH) return 0;
   // sweep + finalize (single GPU) / sweep + reduce + update
@@ -1126,7 +1227,6 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
   if (cfg->row_begin < 0 || cfg->row_end > cfg->m || cfg->row_begin > cfg->row_end)
     return OTDR_E_DIMENSION;
   if (nranks == 1 && (cfg->row_begin != 0 || cfg->row_end != cfg->m)) return OTDR_E_DIMENSION;
-  if (nranks > 1 && !cfg->nccl_id) return OTDR_E_INVALID_ARG;
   if (!otdr_dev_cuda_available()) return OTDR_E_CUDA;
   otdr_dev* ctx = new otdr_dev();
   ctx->cfg = *cfg;
@@ -1217,7 +1317,7 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     CK(cudaMemcpy(ctx->psi, pad.data(), size_t(ctx->ld) * 8, cudaMemcpyHostToDevice));
     ctx->sharded = nranks > 1 || cfg->nccl_id != nullptr;
     ctx->build_segments();
-    if (ctx->sharded) {  // a 1-rank communicator exercises the multi-GPU path on one GPU
+    if (ctx->sharded && cfg->nccl_id) {  // a 1-rank communicator exercises the multi-GPU path on one GPU
       ncclUniqueId id;
       std::memcpy(&id, cfg->nccl_id, sizeof(id));
       NK(nccl().CommInitRank(&ctx->comm, nranks, id, cfg->rank));

@@ -60,7 +60,46 @@ struct StreamArgs {
   int stripes, ntiles;
   long long iters;        // raw mode (prm.solving == 0): iterations to run
   unsigned long long* tstamp;  // optional phase timestamps [kTraceIters][P + 8] (debug)
+  // Row-sharded runs: the exchange goes over peer memory (NVLink P2P) inside
+  // this kernel. peers[r] = rank r's receive buffer (mapped here), layout
+  // [2 parities][nranks][n + 4] doubles then [2][nranks] u64 flags.
+  long long m_glob;
+  double* const* peers;   // nullptr: single GPU
+  double* rbuf;           // this rank's receive buffer (== peers[rank])
+  unsigned long long* xep;  // exchange epoch (monotonic, identical on every rank)
+  int rank, nranks;
 };
+
+// ---- peer-memory exchange helpers (system scope)
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double* xslot(double* buf, int par, int src, int nranks, long long n) {
+  return buf + ((long long)par * nranks + src) * (n + 4);
+}
+__device__ __forceinline__ unsigned long long* xflag(double* buf, int par, int src, int nranks,
+                                                     long long n) {
+  return reinterpret_cast<unsigned long long*>(buf + 2LL * nranks * (n + 4)) + par * nranks + src;
+}
+// publish this rank's contribution of epoch e: caller has fenced its data
+// stores at system scope; one thread per CTA-group calls this.
+__device__ __forceinline__ void xpublish(double* const* peers, int rank, int nranks, long long n,
+                                         unsigned long long e) {
+  __threadfence_system();
+  for (int r = 0; r < nranks; ++r) st_release_sys(xflag(peers[r], int(e & 1), rank, nranks, n), e);
+}
+__device__ __forceinline__ void xwait(double* rbuf, int nranks, long long n, unsigned long long e) {
+  for (int r = 0; r < nranks; ++r) {
+    const unsigned long long* f = xflag(rbuf, int(e & 1), r, nranks, n);
+    while (ld_acquire_sys(f) < e) {
+    }
+  }
+}
 constexpr int kTraceIters = 4;
 
 constexpr int kStreamTN = 256;
@@ -302,7 +341,7 @@ __device__ __forceinline__ void stream_segment_async(const StreamArgs& A, int ti
 // partials in tile order: S_j -> s_j = S_j - q_j, and the stripe's sum of
 // s_j^2 (column folds leave the critical path except for the last stripes).
 __device__ __forceinline__ void stream_stripe_done(const StreamArgs& A, long long stripe,
-                                                   double* sred, bool* s_last) {
+                                                   double* sred, bool* s_last, int par) {
   __threadfence();  // this thread's colpart stores
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -320,9 +359,18 @@ __device__ __forceinline__ void stream_stripe_done(const StreamArgs& A, long lon
     double S = 0.0;
 #pragma unroll 16
     for (int t = t0; t < t1; ++t) S += __ldcg(src + (long long)t * kStreamTN);
-    const double sj = __dsub_rn(S, A.q[j]);
-    A.s[j] = sj;
-    ss = sj * sj;
+    if (A.peers) {  // local column sums to every rank's receive slot (NVLink stores)
+      for (int r = 0; r < A.nranks; ++r) xslot(A.peers[r], par, A.rank, A.nranks, A.n)[j] = S;
+      __threadfence_system();
+    } else {
+      const double sj = __dsub_rn(S, A.q[j]);
+      A.s[j] = sj;
+      ss = sj * sj;
+    }
+  }
+  if (A.peers) {
+    if (threadIdx.x == 0) A.scnt[stripe] = 0;
+    return;
   }
   const double tot = block_sum(ss, sred);
   if (threadIdx.x == 0) {
@@ -351,13 +399,16 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
   const long long gtid = (long long)c * kThreads + threadIdx.x, nthr = (long long)P * kThreads;
 
   const double rho = prm.rho, qd = prm.quad_d, qinv = prm.quad_inv;
-  const double dm = (double)m, dn = (double)n, mn = (double)(m + n);
+  const double dm = (double)A.m_glob, dn = (double)n, mn = (double)(A.m_glob + n);
   long long k = ctl->k;
   double theta = ctl->theta[k & 1];
   double best = ctl->best;
   long long last_imp = ctl->last_improvement;
   const long long k0 = ctl->k0;
   long long it = 0;
+  const bool peer = A.peers != nullptr;
+  const unsigned long long ebase = peer ? *A.xep : 0ull;
+  unsigned long long epoch = ebase + 1;
 
   auto stamp = [&](int slot) {
     if (A.tstamp && it < kTraceIters && threadIdx.x == 0 && (slot < P ? true : c == 0))
@@ -377,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
       } else {
         stream_segment<T, REG, EXACT, NV, U>(A, tile, tl.x, tl.y, tl.z, rho, qd, qinv, red);
       }
-      stream_stripe_done(A, tl.x, sred, &s_last);
+      stream_stripe_done(A, tl.x, sred, &s_last, int(epoch & 1));
     }
     stamp(c);
     grid_barrier(&ctl->bar_str);
@@ -421,7 +472,62 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
     stamp(P + 3);
 
     // ---- C. scalar folds (same order in every CTA), recurrence, stopping
-    if (warp < 3) {
+    if (peer) {
+      // exchange: CTA 0 sends this rank's (sum r, sum r^2, sum R) and the
+      // epoch flags; every CTA waits for all ranks, then folds in rank order
+      if (c == 0 && warp < 3) {
+        double u = 0.0;
+        for (int cc = lane; cc < P; cc += 32) u += __ldcg(A.part + cc * 4 + warp);
+        u = warp_sum(u);
+        if (lane == 0) {
+          for (int r = 0; r < A.nranks; ++r)
+            xslot(A.peers[r], int(epoch & 1), A.rank, A.nranks, n)[n + warp] = u;
+          __threadfence_system();
+        }
+      }
+      if (c == 0) {
+        __syncthreads();
+        if (threadIdx.x == 0) xpublish(A.peers, A.rank, A.nranks, n, epoch);
+      }
+      if (threadIdx.x == 0) xwait(A.rbuf, A.nranks, n, epoch);
+      __syncthreads();
+      if (warp < 3) {
+        double u = 0.0;
+        if (lane == 0)
+          for (int r = 0; r < A.nranks; ++r)
+            u += __ldcg(xslot(A.rbuf, int(epoch & 1), r, A.nranks, n) + n + warp);
+        if (lane == 0) bc[warp] = u;
+      }
+      __syncthreads();
+      if (c == 0 && threadIdx.x == 0) ctl->tile_ctr = 0;
+      const double eta_p = __ddiv_rn(bc[0], mn);
+      const double shift_p = __dsub_rn(2.0 * eta_p, theta);
+      double ssq = 0.0;
+      for (long long j = gtid; j < n; j += nthr) {
+        double S = 0.0;
+        for (int r = 0; r < A.nranks; ++r) S += __ldcg(xslot(A.rbuf, int(epoch & 1), r, A.nranks, n) + j);
+        const double sj = __dsub_rn(S, A.q[j]), bj = A.b[j];
+        A.s[j] = sj;
+        ssq += sj * sj;
+        A.psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift_p), dm);
+        A.b[j] = __dsub_rn(bj, sj);
+      }
+      for (long long i = gtid; i < m; i += nthr) {
+        const double ri = __ldcg(A.r + i), ai = A.a[i];
+        A.phi[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift_p), dn);
+        A.a[i] = __dsub_rn(ai, ri);
+      }
+      const double t4 = block_sum(ssq, sred);
+      if (threadIdx.x == 0) A.part[c * 4 + 3] = t4;
+      grid_barrier(&ctl->bar_str);  // phi / psi / s complete, ssq partials visible
+      if (warp == 0) {
+        double u = 0.0;
+        for (int cc = lane; cc < P; cc += 32) u += __ldcg(A.part + cc * 4 + 3);
+        u = warp_sum(u);
+        if (lane == 0) bc[3] = u;
+      }
+      __syncthreads();
+    } else if (warp < 3) {
       double u = 0.0;
       for (int cc = lane; cc < P; cc += 32) u += __ldcg(A.part + cc * 4 + warp);
       u = warp_sum(u);
@@ -432,26 +538,30 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
       u = warp_sum(u);
       if (lane == 0) bc[3] = u;
     }
-    __syncthreads();
-    if (c == 0 && threadIdx.x == 0) ctl->tile_ctr = 0;  // every CTA is past its last claim
+    if (!peer) {
+      __syncthreads();
+      if (c == 0 && threadIdx.x == 0) ctl->tile_ctr = 0;  // every CTA is past its last claim
+      const double eta_l = __ddiv_rn(bc[0], mn);
+      const double shift_l = __dsub_rn(2.0 * eta_l, theta);
+      for (long long i = gtid; i < m; i += nthr) {
+        const double ri = __ldcg(A.r + i), ai = A.a[i];
+        A.phi[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift_l), dn);
+        A.a[i] = __dsub_rn(ai, ri);
+      }
+      for (long long j = gtid; j < n; j += nthr) {
+        const double sj = __ldcg(A.s + j), bj = A.b[j];
+        A.psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift_l), dm);
+        A.b[j] = __dsub_rn(bj, sj);
+      }
+    }
     const double eta = __ddiv_rn(bc[0], mn);
-    const double shift = __dsub_rn(2.0 * eta, theta);
-    for (long long i = gtid; i < m; i += nthr) {
-      const double ri = __ldcg(A.r + i), ai = A.a[i];
-      A.phi[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift), dn);
-      A.a[i] = __dsub_rn(ai, ri);
-    }
-    for (long long j = gtid; j < n; j += nthr) {
-      const double sj = __ldcg(A.s + j), bj = A.b[j];
-      A.psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift), dm);
-      A.b[j] = __dsub_rn(bj, sj);
-    }
     stamp(P + 4);
     const double nr2 = sqrt(bc[1]), ns2 = sqrt(bc[3]);
     const double rp = (nr2 < ns2) ? ns2 : nr2;  // std::max semantics (solver.cpp:179)
     theta = __dsub_rn(theta, eta);
     ++k;
     ++it;
+    ++epoch;
     const long long kk = k - k0;
     bool done = false;
     int term = TERM_MAXITER;
@@ -491,11 +601,43 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
           ctl->done = 1;
           ctl->termination = term;
         }
+        if (peer) *A.xep = epoch - 1;  // every CTA read the base at entry
       }
       break;
     }
-    grid_barrier(&ctl->bar_str);  // phi / psi complete before the next sweep
+    if (!peer) grid_barrier(&ctl->bar_str);  // phi / psi complete before the next sweep
   }
+}
+
+// Small all-reduce (sum) of `count` <= n + 4 doubles over peer memory, for the
+// non-hot exchanges of row-sharded runs (make_state sums, certificate / objective
+// partials, the group-lasso graph path): one CTA writes the vector into every
+// rank's receive slot, publishes the epoch flag, waits for every rank and sums
+// in rank order -- identical results on every rank.
+__global__ void __launch_bounds__(1024) p2p_allreduce_kernel(double* buf, long long count,
+                                                             double* const* peers, double* rbuf,
+                                                             unsigned long long* xep, int rank,
+                                                             int nranks, long long n) {
+  const unsigned long long e = *xep + 1;
+  const int par = int(e & 1);
+  for (long long t = threadIdx.x; t < count; t += blockDim.x) {
+    const double v = buf[t];
+    for (int r = 0; r < nranks; ++r) xslot(peers[r], par, rank, nranks, n)[t] = v;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    xpublish(peers, rank, nranks, n, e);
+    xwait(rbuf, nranks, n, e);
+  }
+  __syncthreads();
+  for (long long t = threadIdx.x; t < count; t += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < nranks; ++r) s += __ldcg(xslot(rbuf, par, r, nranks, n) + t);
+    buf[t] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *xep = e;
 }
 
 }  // namespace otdrk

@@ -394,7 +394,7 @@ class Shard:
     nranks: int
     row_begin: int
     row_end: int
-    nccl_id: bytes
+    nccl_id: Optional[bytes] = None  # None: exchange over peer memory only (Engine.peer_*)
 
 
 def default_stepsize(m: int, n: int) -> float:  # solver.cpp:55-57
@@ -583,6 +583,19 @@ class Engine:
         self._ck(self._L.otdr_dev_time_steps(self._h, float(rho), int(iters), ct.byref(ms)))
         return ms.value
 
+    # -- peer-memory exchange of row-sharded runs (CUDA IPC over NVLink)
+    def peer_export(self) -> bytes:
+        """This rank's receive-buffer IPC handle (all-gather it across ranks)."""
+        buf = ct.create_string_buffer(nat.PEER_HANDLE_BYTES)
+        self._ck(self._L.otdr_dev_peer_export(self._h, buf))
+        return buf.raw
+
+    def peer_import(self, handles) -> None:
+        """Open every rank's handle (rank order); the solve loop then exchanges
+        column sums over peer memory inside the streaming kernel."""
+        blob = b"".join(handles)
+        self._ck(self._L.otdr_dev_peer_import(self._h, blob))
+
     def kernels_per_iteration(self) -> int:
         """Launches per DR iteration on the graph path; 0 for persistent loops."""
         return self._L.otdr_dev_kernels_per_iteration(self._h)
@@ -590,6 +603,17 @@ class Engine:
     def solve_path(self) -> str:
         """Device loop used by step()/solve(): "graph", "resident" or "stream"."""
         return ("graph", "resident", "stream")[self._L.otdr_dev_solve_path(self._h)]
+
+
+def link_local(engines) -> None:
+    """Link the rank contexts of ONE process (engines[r] = rank r) for the
+    peer-memory exchange -- the multi-rank path on one GPU (tests)."""
+    L = nat.lib()
+    arr = (ct.c_void_p * len(engines))(*[e._h for e in engines])
+    rc = L.otdr_dev_peer_link_local(arr, len(engines))
+    if rc != nat.OTDR_OK:
+        msg = L.otdr_dev_last_error(engines[0]._h).decode(errors="replace")
+        raise _ERRORS.get(rc, DeviceError)(msg or nat.STATUS_NAMES.get(rc, str(rc)))
 
 
 class BatchEngine:

@@ -1,10 +1,14 @@
 """Row sharding of the plan across GPUs (one process per GPU).
 
 Rank r owns a contiguous band of plan rows. Per DR iteration each rank sweeps
-its band (row sums complete locally), then ONE ncclAllReduce of the n+3 vector
-[column sums | sum r | sum r^2 | sum X] gives every rank the global column sums
-and residual scalars; every rank then updates the replicated column-side
-vectors (psi, b, s) and its own rows of (phi, a) identically.
+its band (row sums complete locally) and the n+3 vector [column sums | sum r |
+sum r^2 | sum X] is all-reduced; every rank then updates the replicated
+column-side vectors (psi, b, s) and its own rows of (phi, a) identically
+(SURVEY §8(e)). With peers linked (connect_peers, CUDA IPC) the exchange runs
+inside the streaming kernel over NVLink: each stripe's column sums are stored
+into every rank's receive buffer as soon as the stripe is swept (overlapped
+with the rest of the sweep), and epoch flags at system scope order the fold.
+Without a peer link, one ncclAllReduce per iteration between kernels.
 
 Group lasso: a group is (column, class), so a class's rows must all live on
 one rank for its norms to stay local -- bands are cut at class boundaries and a
@@ -70,10 +74,34 @@ def broadcast_nccl_id(dist, rank: int) -> bytes:
     return obj[0]
 
 
+def connect_peers(dist, eng: Engine) -> bool:
+    """All-gather every rank's receive-buffer IPC handle and import them, so
+    the solve loop exchanges column sums over NVLink peer memory inside the
+    streaming kernel (collective). Returns False -- keeping the NCCL
+    exchange -- when a peer's buffer cannot be mapped (no P2P path)."""
+    handles = [None] * dist.get_world_size()
+    dist.all_gather_object(handles, eng.peer_export())
+    try:
+        eng.peer_import(handles)
+        ok = 1
+    except Exception:
+        ok = 0
+    flags = [None] * dist.get_world_size()
+    dist.all_gather_object(flags, ok)
+    if not all(flags):
+        raise RuntimeError("peer-memory exchange could not be set up on every rank")
+    return True
+
+
 def open_sharded_engine(dist, m: int, n: int, storage: str = "f32", device: int = 0,
-                        labels: Optional[Sequence[int]] = None) -> Tuple[Engine, int, int]:
-    """Engine over this rank's band (collective: every rank must call it)."""
+                        labels: Optional[Sequence[int]] = None,
+                        peers: bool = True) -> Tuple[Engine, int, int]:
+    """Engine over this rank's band (collective: every rank must call it).
+    peers=True links the ranks' receive buffers for the in-kernel exchange."""
     rank, world = dist.get_rank(), dist.get_world_size()
     lo, hi = row_bands(m, world, labels)[rank]
     nid = broadcast_nccl_id(dist, rank)
-    return Engine(m, n, storage, device=device, shard=Shard(rank, world, lo, hi, nid)), lo, hi
+    eng = Engine(m, n, storage, device=device, shard=Shard(rank, world, lo, hi, nid))
+    if peers and world > 1:
+        connect_peers(dist, eng)
+    return eng, lo, hi

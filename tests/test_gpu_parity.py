@@ -643,3 +643,85 @@ def test_stream_kernel_matches_graph_loop(ora, monkeypatch, storage):
     assert a[1].termination == b[1].termination
     assert abs(a[1].iterations - b[1].iterations) <= (0 if storage == "f64" else 2)
     assert abs(a[1].objective - b[1].objective) <= (1e-9 if storage == "f64" else 1e-6) * abs(b[1].objective)
+
+
+def _parallel(fns):
+    """Run one callable per rank concurrently (ctypes releases the GIL), so
+    every rank's exchange kernel is in flight at the same time."""
+    import threading
+
+    out, err = [None] * len(fns), []
+
+    def run(i):
+        try:
+            out[i] = fns[i]()
+        except BaseException as e:  # pragma: no cover - reported below
+            err.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(len(fns))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in th), "a rank hung in the exchange"
+    if err:
+        raise err[0]
+    return out
+
+
+@pytest.mark.parametrize("storage", ["f64", "f32"])
+@pytest.mark.parametrize("world,kind", [(2, "quad"), (3, "none")])
+def test_peer_exchange_ranks_on_one_gpu(ora, monkeypatch, storage, world, kind):
+    """Row-sharded run with the in-kernel peer-memory exchange: `world` rank
+    contexts on one GPU, linked in-process, each running the streaming kernel
+    (grid capped so all ranks' kernels are co-resident). Iterates match the
+    unsharded oracle; solve() stops at the same iteration on every rank."""
+    monkeypatch.setenv("OTDR_STREAM_GRID", str(240 // world))
+    from paper_2305_18483_b200 import sharding
+
+    m, n = 900, 700
+    C, p, q, *_ = ora.gaussian_problem(m, n, 31)
+    Co = C if storage == "f64" else C.astype(np.float32).astype(np.float64)
+    param = 5e-3 * (m + n) if kind == "quad" else 0.0
+    pr = ora.Problem(Co, p, q)
+    oreg = oracle_reg(ora, kind, param, None, n)
+    st = ora.make_state(pr)
+    bands = sharding.row_bands(m, world)
+    engs = []
+    for r, (lo, hi) in enumerate(bands):
+        e = otdr.Engine(m, n, storage, shard=otdr.Shard(r, world, lo, hi, None))
+        e.set_problem(C[lo:hi], p[lo:hi], q)
+        e.set_regularizer(dev_reg(kind, param, None, n))
+        engs.append(e)
+    otdr.link_local(engs)
+    assert all(e.solve_path() == "stream" for e in engs)
+    _parallel([e.set_state for e in engs])
+    rho = ora.default_stepsize(m, n)
+    tol = 1e-12 if storage == "f64" else 1e-5
+    done = 0
+    for k in (1, 9, 30):
+        for _ in range(k - done):
+            ora.step(st, pr, oreg, rho)
+        _parallel([lambda e=e: e.step(rho, k - done) for e in engs])
+        done = k
+        gs = _parallel([e.get_state for e in engs])
+        X = np.concatenate([g.X for g in gs])
+        phi = np.concatenate([g.phi for g in gs])
+        assert rel(X, st.X) <= tol, (k, rel(X, st.X))
+        assert rel(phi, st.phi) <= tol
+        for g in gs:
+            assert g.k == k
+            assert rel(g.psi, st.psi) <= tol and rel(g.b, st.b) <= tol
+            assert abs(g.theta - st.theta) <= (1e-12 if storage == "f64" else 1e-9) * max(1.0, abs(st.theta))
+    _parallel([e.set_state for e in engs])
+    o = ora.solve(pr, oreg, tol_primal=1e-6, max_iter=4000)
+    reps = _parallel([lambda e=e: e.solve(otdr.SolverOptions(tol_primal=1e-6, max_iter=4000,
+                                                             storage=storage), with_state=False)
+                      for e in engs])
+    for rep in reps:
+        assert rep.termination.name == o.termination
+        assert abs(rep.iterations - o.iterations) <= (0 if storage == "f64" else 2)
+        assert abs(rep.r_primal - reps[0].r_primal) == 0.0
+        assert abs(rep.objective - o.objective) <= (1e-9 if storage == "f64" else 1e-6) * abs(o.objective)
+    for e in engs:
+        e.close()

@@ -1,0 +1,30 @@
+"""Two processes on one GPU as the two ranks of a row-sharded run, exchanging
+over CUDA IPC peer memory inside the streaming kernel (the multi-GPU path of
+bench.py --gpus N, minus NVLink). The two contexts time-slice the GPU."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def test_peer_ipc_two_processes():
+    env = dict(os.environ, OTDR_STREAM_GRID="64")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tests", "_peer_ipc_worker.py")]
+    out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=240)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-4000:]
+    assert "PEER_IPC_OK" in out.stdout, out.stdout[-2000:]
