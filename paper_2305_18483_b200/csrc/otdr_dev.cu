@@ -137,7 +137,7 @@ struct otdr_dev {
   std::vector<void*> ipc_opened;
   // persistent streaming solve (single GPU, zero / quadratic, HBM-resident plan)
   bool allow_stream = true;
-  int str_P = 0, str_ntiles = 0, str_tpc = 8, str_tail = 2;
+  int str_P = 0, str_ntiles = 0, str_tpc = 8, str_tail = 4;
   double *str_part = nullptr, *str_colpart = nullptr;
   int4* d_tiles = nullptr;
   int* d_sfirst = nullptr;
@@ -610,7 +610,10 @@ struct otdr_dev {
     // stripes, about two rounds of long tiles' worth of rows
     // about str_tpc long tiles per CTA (OTDR_STREAM_TILES)
     const long long big = std::max<long long>(16, (m_loc * S + str_tpc * P - 1) / (str_tpc * P));
-    const long long small = std::max<long long>(32, big / std::max(1, str_tail));
+    // short tail tiles: a quarter of a long tile, but >= 96 rows (smaller tiles
+    // cost more in per-tile pipeline fill than they save in tail; measured at
+    // 10000^2 and 20000^2)
+    const long long small = std::min(big, std::max<long long>(96, big / std::max(1, str_tail)));
     const long long tail_stripes =
         str_tail > 1 ? std::min<long long>(S, (P * big + m_loc - 1) / m_loc) : 0;
     std::vector<int4> tiles;
