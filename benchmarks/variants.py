@@ -21,9 +21,9 @@ import torch
 import paper_2305_18483_b200 as otdr
 from paper_2305_18483_b200 import datagen
 cfg = CFG
-if cfg in ("headline", "cfg2", "cfg4"):
-    m = {"headline": 20000, "cfg2": 10000, "cfg4": 40000}[cfg]
-    reg = {"headline": otdr.QuadraticReg(200.0), "cfg2": otdr.ZeroReg(), "cfg4": otdr.QuadraticReg(400.0)}[cfg]
+if cfg in ("headline", "cfg2", "cfg4", "cfg1") or cfg.startswith("n"):
+    m = {"headline": 20000, "cfg2": 10000, "cfg4": 40000, "cfg1": 1000}.get(cfg) or int(cfg[1:])
+    reg = {"cfg2": otdr.ZeroReg()}.get(cfg, otdr.QuadraticReg(5e-3 * 2 * m))
     eng = otdr.Engine(m, m, "f32")
     src, tgt = datagen.gaussian_points(m, m, 0)
     eng.build_sqdist_cost(src, tgt, datagen.uniform(m), datagen.uniform(m))
@@ -40,7 +40,7 @@ eng.step(rho, 5)
 ms = eng.time_steps(rho, ITERS) / ITERS
 prof = eng.profile(rho, 5)
 alg = 12.0 * m * m
-print("RESULT " + json.dumps(dict(cfg=cfg, variant=VARIANT, ms_per_iter=ms, iters_per_s=1e3 / ms,
+print("RESULT " + json.dumps(dict(cfg=cfg, variant=VARIANT, path=eng.solve_path(), ms_per_iter=ms, iters_per_s=1e3 / ms,
       sweep_ms=prof["sweep_ms"], sweep_GBps=alg / prof["sweep_ms"] / 1e6,
       iter_GBps=alg / ms / 1e6, prof=prof)), flush=True)
 """
@@ -48,7 +48,8 @@ print("RESULT " + json.dumps(dict(cfg=cfg, variant=VARIANT, ms_per_iter=ms, iter
 
 def main():
     cfg = sys.argv[1]
-    iters = 100 if cfg != "cfg4" else 30
+    iters = {"cfg4": 30, "cfg1": 2000}.get(cfg, 100 if not cfg.startswith("n") else
+                                          max(30, min(2000, int(4e10 / int(cfg[1:]) ** 2))))
     for var in sys.argv[2:] or ["default"]:
         env = dict(os.environ)
         for kv in var.split(","):

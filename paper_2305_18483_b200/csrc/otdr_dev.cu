@@ -609,7 +609,10 @@ struct otdr_dev {
     // long tiles (the plain sweep's rows_per_cta), short ones for the last
     // stripes, about two rounds of long tiles' worth of rows
     // about str_tpc long tiles per CTA (OTDR_STREAM_TILES)
-    const long long big = std::max<long long>(16, (m_loc * S + str_tpc * P - 1) / (str_tpc * P));
+    // (>= 128 rows: shorter tiles cost more in pipeline fill and partial
+    // folds than they gain in balance -- measured at 4000^2)
+    const long long big = std::min<long long>(
+        std::max<long long>(1, m_loc), std::max<long long>(128, (m_loc * S + str_tpc * P - 1) / (str_tpc * P)));
     // short tail tiles: a quarter of a long tile, but >= 96 rows (smaller tiles
     // cost more in per-tile pipeline fill than they save in tail; measured at
     // 10000^2 and 20000^2)
@@ -799,7 +802,10 @@ struct otdr_dev {
       if (!gk0 || std::strcmp(gk0, "pipe") == 0) {
         int max_smem = 0;
         CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg.device));
+        int dmax = 4;
+        if (const char* gd = std::getenv("OTDR_GL_PIPE_D")) dmax = std::max(2, std::min(4, std::atoi(gd)));
         for (int d : {4, 3, 2}) {
+          if (d > dmax) continue;
           const size_t need = f64() ? otdrk::glpipe_smem_bytes<double, 4>(int(lmax)) -
                                           otdrk::glpipe_queue_bytes<double, 4>() +
                                           size_t(d) * 2 * otdrk::kGLPThreads * 16

@@ -36,7 +36,7 @@ namespace otdrk {
 
 constexpr int kGLPThreads = 512;
 constexpr int kGLPWarps = kGLPThreads / 32;
-constexpr int kGLPMaxG = 8;
+constexpr int kGLPMaxG = 16;
 
 struct GLPipeArgs {
   void* X;
