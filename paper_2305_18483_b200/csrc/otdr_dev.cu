@@ -262,7 +262,10 @@ struct otdr_dev {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(glp_smem)));
     otdrk::GLPipeArgs ga{X, C, phi, psi, rowpart, colpart, d_seg, d_glp_pos, d_prm, d_ctl, m_loc, ld,
                          num_segs, glp_nstr, glp_groups, glp_lmax};
-    kern<<<num_sms, otdrk::kGLPThreads, glp_smem, stream>>>(ga);
+    // OTDR_GL_PIPE_GRID caps the persistent grid (several ranks sharing one GPU in tests)
+    static const int cap = std::getenv("OTDR_GL_PIPE_GRID") ? std::atoi(std::getenv("OTDR_GL_PIPE_GRID")) : 0;
+    const int grid = cap > 0 ? std::min(cap, num_sms) : num_sms;
+    kern<<<grid, otdrk::kGLPThreads, glp_smem, stream>>>(ga);
   }
   void launch_gl_pipe() {
     if (f64()) {
@@ -421,7 +424,7 @@ struct otdr_dev {
     if (comm) {
       NK(nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, comm, stream));
     } else if (p2p) {
-      otdrk::p2p_allreduce_kernel<<<1, 1024, 0, stream>>>(buf, (long long)count, d_peers, rbuf, d_xep,
+      otdrk::p2p_allreduce_kernel<<<1, 512, 0, stream>>>(buf, (long long)count, d_peers, rbuf, d_xep,
                                                           cfg.rank, cfg.nranks, n);
     } else if (cfg.nranks > 1) {
       throw Error{OTDR_E_STATE, "row-sharded context has no exchange: pass an NCCL id or link peers"};
@@ -438,7 +441,82 @@ struct otdr_dev {
     d_xep = dalloc<unsigned long long>(1);
     CK(cudaMemset(d_xep, 0, 8));
   }
+  // Under lazy module loading (CUDA 12 default) the first launch of a kernel
+  // waits for the device to idle. Ranks that share ONE GPU (the multi-context
+  // tests) would deadlock: a rank's exchange kernel spins until the other rank
+  // launches, and that launch waits for the spinning kernel. Load every kernel
+  // a sharded context can launch before the first exchange.
+  template <typename K>
+  static void touch(K k) {
+    cudaFuncAttributes at;
+    CK(cudaFuncGetAttributes(&at, reinterpret_cast<const void*>(k)));
+  }
+  template <typename T, int REG>
+  static void touch_stream() {
+    constexpr bool E = sizeof(T) == 8;
+    constexpr int NV = E ? 4 : 2, U = E ? 1 : 2;
+    touch(otdrk::stream_kernel<T, REG, E, NV, U, 0>);
+    touch(otdrk::stream_kernel<T, REG, E, NV, U, 2>);
+    touch(otdrk::stream_kernel<T, REG, E, NV, U, 3>);
+    touch(otdrk::stream_kernel<T, REG, E, NV, U, 4>);
+    touch(otdrk::stream_kernel<T, REG, E, NV, U, 5>);
+  }
+  static void preload_kernels() {
+    static bool done = false;
+    if (done) return;
+    touch(otdrk::p2p_allreduce_kernel);
+    touch_stream<float, otdrk::REG_NONE>();
+    touch_stream<float, otdrk::REG_QUAD>();
+    touch_stream<double, otdrk::REG_NONE>();
+    touch_stream<double, otdrk::REG_QUAD>();
+    touch(otdrk::sweep_kernel<double, otdrk::REG_NONE, true, false, 4, 1>);
+    touch(otdrk::sweep_kernel<double, otdrk::REG_NONE, true, true, 4, 1>);
+    touch(otdrk::sweep_kernel<double, otdrk::REG_QUAD, true, false, 4, 1>);
+    touch(otdrk::sweep_kernel<double, otdrk::REG_QUAD, true, true, 4, 1>);
+    touch(otdrk::sweep_kernel<float, otdrk::REG_NONE, false, false, 2, 2>);
+    touch(otdrk::sweep_kernel<float, otdrk::REG_NONE, false, true, 2, 2>);
+    touch(otdrk::sweep_kernel<float, otdrk::REG_QUAD, false, false, 2, 2>);
+    touch(otdrk::sweep_kernel<float, otdrk::REG_QUAD, false, true, 2, 2>);
+    touch(otdrk::gl_pipe_kernel<float, false, 2>);
+    touch(otdrk::gl_pipe_kernel<float, false, 3>);
+    touch(otdrk::gl_pipe_kernel<float, false, 4>);
+    touch(otdrk::gl_pipe_kernel<double, true, 2>);
+    touch(otdrk::gl_pipe_kernel<double, true, 3>);
+    touch(otdrk::gl_pipe_kernel<double, true, 4>);
+    touch(otdrk::gl_ring_kernel<float, false>);
+    touch(otdrk::gl_ring_kernel<double, true>);
+    touch(otdrk::gl_stage_kernel<float, false>);
+    touch(otdrk::gl_stage_kernel<double, true>);
+    touch(otdrk::gl_sweep_kernel<double, true, false, 1>);
+    touch(otdrk::gl_sweep_kernel<double, true, true, 1>);
+    touch(otdrk::gl_sweep_kernel<float, false, false, 1>);
+    touch(otdrk::gl_sweep_kernel<float, false, true, 1>);
+    touch(otdrk::gl_cluster_kernel<float, false, 4, kGLThreads>);
+    touch(otdrk::gl_cluster_kernel<float, false, 2, kGLThreads>);
+    touch(otdrk::gl_cluster_kernel<double, true, 2, kGLThreads>);
+    touch(otdrk::gl_cluster_kernel<double, true, 1, kGLThreads>);
+    touch(otdrk::reduce_kernel);
+    touch(otdrk::update_kernel);
+    touch(otdrk::finalize_kernel);
+    touch(otdrk::seed_state_kernel);
+    touch(otdrk::stamp_t0_kernel);
+    touch(otdrk::cert_partial_kernel<double, 1>);
+    touch(otdrk::cert_partial_kernel<float, 1>);
+    touch(otdrk::cert_final_kernel);
+    touch(otdrk::unshift_kernel<double>);
+    touch(otdrk::unshift_kernel<float>);
+    touch(otdrk::scatter_rows_kernel<double>);
+    touch(otdrk::scatter_rows_kernel<float>);
+    touch(otdrk::gather_rows_kernel<double>);
+    touch(otdrk::gather_rows_kernel<float>);
+    touch(otdrk::move_rows_kernel);
+    touch(otdrk::sqdist_kernel<double>);
+    touch(otdrk::sqdist_kernel<float>);
+    done = true;
+  }
+
   void set_peers(const std::vector<double*>& peers) {
+    preload_kernels();
     if (!d_peers) d_peers = dalloc<double*>(size_t(cfg.nranks));
     CK(cudaMemcpy(d_peers, peers.data(), size_t(cfg.nranks) * sizeof(double*), cudaMemcpyHostToDevice));
     p2p = true;

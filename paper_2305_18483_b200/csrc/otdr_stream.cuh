@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
 // partials, the group-lasso graph path): one CTA writes the vector into every
 // rank's receive slot, publishes the epoch flag, waits for every rank and sums
 // in rank order -- identical results on every rank.
-__global__ void __launch_bounds__(1024) p2p_allreduce_kernel(double* buf, long long count,
+__global__ void __launch_bounds__(512) p2p_allreduce_kernel(double* buf, long long count,
                                                              double* const* peers, double* rbuf,
                                                              unsigned long long* xep, int rank,
                                                              int nranks, long long n) {

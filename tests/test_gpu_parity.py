@@ -725,3 +725,42 @@ def test_peer_exchange_ranks_on_one_gpu(ora, monkeypatch, storage, world, kind):
         assert abs(rep.objective - o.objective) <= (1e-9 if storage == "f64" else 1e-6) * abs(o.objective)
     for e in engs:
         e.close()
+
+
+def test_peer_exchange_group_lasso_graph_path(ora, monkeypatch):
+    """Group lasso on two rank contexts of one process, peers linked, no NCCL:
+    the graph loop's per-iteration exchange runs through p2p_allreduce_kernel.
+    Bands are cut at class boundaries; iterates match the unsharded oracle.
+    (The persistent GL grid is capped so a rank's spinning exchange kernel
+    never holds the SM the other rank's sweep still needs -- one GPU only.)"""
+    monkeypatch.setenv("OTDR_GL_PIPE_GRID", "100")
+    from paper_2305_18483_b200 import sharding
+
+    m, n, classes = 1200, 500, 4
+    C, p, q, src, tgt, ls, lt = ora.adaptation_problem(m, n, classes, 5)
+    pr = ora.Problem(C, p, q)
+    offs, cells = ora.column_class_blocks(ls, n)
+    oreg = ora.group_lasso_reg(2e-3, offs, cells)
+    st = ora.make_state(pr)
+    bands = sharding.row_bands(m, 2, ls)
+    engs = []
+    for r, (lo, hi) in enumerate(bands):
+        e = otdr.Engine(m, n, "f64", shard=otdr.Shard(r, 2, lo, hi, None))
+        e.set_problem(C[lo:hi], p[lo:hi], q)
+        e.set_regularizer(otdr.GroupLassoReg(2e-3, otdr.column_class_blocks(ls, n)),
+                          labels_local=np.asarray(ls)[lo:hi])
+        engs.append(e)
+    otdr.link_local(engs)
+    assert all(e.solve_path() == "graph" for e in engs)
+    _parallel([e.set_state for e in engs])
+    rho = ora.default_stepsize(m, n)
+    for _ in range(15):
+        ora.step(st, pr, oreg, rho)
+    _parallel([lambda e=e: e.step(rho, 15) for e in engs])
+    gs = _parallel([e.get_state for e in engs])
+    X = np.concatenate([g.X for g in gs])
+    assert rel(X, st.X) <= 1e-12, rel(X, st.X)
+    assert rel(np.concatenate([g.phi for g in gs]), st.phi) <= 1e-12
+    assert all(rel(g.psi, st.psi) <= 1e-12 for g in gs)
+    for e in engs:
+        e.close()
