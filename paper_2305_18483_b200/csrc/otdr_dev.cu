@@ -520,6 +520,8 @@ struct otdr_dev {
     if (!d_peers) d_peers = dalloc<double*>(size_t(cfg.nranks));
     CK(cudaMemcpy(d_peers, peers.data(), size_t(cfg.nranks) * sizeof(double*), cudaMemcpyHostToDevice));
     p2p = true;
+    sharded = true;  // a linked 1-rank context runs the sharded (peer-exchange) loop
+    res_G = 0;
     invalidate_graphs();
     plan_stream();
   }
@@ -689,12 +691,13 @@ struct otdr_dev {
     // about str_tpc long tiles per CTA (OTDR_STREAM_TILES)
     // (>= 128 rows: shorter tiles cost more in pipeline fill and partial
     // folds than they gain in balance -- measured at 4000^2)
+    static const long long min_rows = std::getenv("OTDR_STREAM_MINROWS") ? std::atoll(std::getenv("OTDR_STREAM_MINROWS")) : 128;
     const long long big = std::min<long long>(
-        std::max<long long>(1, m_loc), std::max<long long>(128, (m_loc * S + str_tpc * P - 1) / (str_tpc * P)));
+        std::max<long long>(1, m_loc), std::max<long long>(min_rows, (m_loc * S + str_tpc * P - 1) / (str_tpc * P)));
     // short tail tiles: a quarter of a long tile, but >= 96 rows (smaller tiles
     // cost more in per-tile pipeline fill than they save in tail; measured at
     // 10000^2 and 20000^2)
-    const long long small = std::min(big, std::max<long long>(96, big / std::max(1, str_tail)));
+    const long long small = std::min(big, std::max<long long>(std::min<long long>(96, min_rows), big / std::max(1, str_tail)));
     const long long tail_stripes =
         str_tail > 1 ? std::min<long long>(S, (P * big + m_loc - 1) / m_loc) : 0;
     std::vector<int4> tiles;
@@ -776,7 +779,7 @@ struct otdr_dev {
                          cfg.rank, cfg.nranks};
     static const bool trace = std::getenv("OTDR_STREAM_TRACE") != nullptr;
     unsigned long long* ts = nullptr;
-    const size_t tsn = size_t(otdrk::kTraceIters) * size_t(str_P + 8);
+    const size_t tsn = size_t(otdrk::kTraceIters) * size_t(str_P + 12);
     if (trace) {
       ts = dalloc<unsigned long long>(tsn);
       CK(cudaMemset(ts, 0, tsn * 8));
@@ -798,7 +801,7 @@ struct otdr_dev {
       CK(cudaMemcpy(h.data(), ts, tsn * 8, cudaMemcpyDeviceToHost));
       cudaFree(ts);
       for (int it = 0; it < otdrk::kTraceIters; ++it) {
-        const unsigned long long* row = h.data() + size_t(it) * size_t(str_P + 8);
+        const unsigned long long* row = h.data() + size_t(it) * size_t(str_P + 12);
         const unsigned long long t0 = row[str_P];
         if (!t0) break;
         unsigned long long mn = ~0ull, mx = 0;
@@ -812,6 +815,10 @@ struct otdr_dev {
                      (row[str_P + 5] - t0) * 1e-3, (row[str_P + 6] - t0) * 1e-3,
                      (row[str_P + 2] - t0) * 1e-3, (row[str_P + 3] - t0) * 1e-3,
                      (row[str_P + 4] - t0) * 1e-3);
+        if (row[str_P + 8])
+          std::fprintf(stderr, "   peer: published %.1f waited %.1f cols+rows %.1f bar %.1f\n",
+                       (row[str_P + 8] - t0) * 1e-3, (row[str_P + 9] - t0) * 1e-3,
+                       (row[str_P + 10] - t0) * 1e-3, (row[str_P + 11] - t0) * 1e-3);
         if (it == 1) {
           std::vector<double> dv(static_cast<size_t>(str_P));
           for (int c = 0; c < str_P; ++c) dv[size_t(c)] = (row[c] - t0) * 1e-3;
@@ -1251,7 +1258,6 @@ otdr_status otdr_dev_peer_export(otdr_dev* ctx, void* handle) {
 
 otdr_status otdr_dev_peer_import(otdr_dev* ctx, const void* handles) {
   if (!ctx || !handles) return OTDR_E_INVALID_ARG;
-  if (!ctx->sharded) return fail(ctx, OTDR_E_STATE, "peer exchange needs a row-sharded context");
   return guarded(ctx, [&] {
     ctx->alloc_rbuf();
     const int nr = ctx->cfg.nranks;
@@ -1278,7 +1284,7 @@ otdr_status otdr_dev_peer_link_local(otdr_dev** ctxs, int nranks) {
   if (!ctxs || nranks < 1) return OTDR_E_INVALID_ARG;
   for (int r = 0; r < nranks; ++r) {
     if (!ctxs[r]) return OTDR_E_INVALID_ARG;
-    if (ctxs[r]->cfg.nranks != nranks || ctxs[r]->cfg.rank != r || !ctxs[r]->sharded)
+    if (ctxs[r]->cfg.nranks != nranks || ctxs[r]->cfg.rank != r || (nranks > 1 && !ctxs[r]->sharded))
       return fail(ctxs[r], OTDR_E_STATE, "contexts must be the ranks 0..nranks-1 of one sharded run");
   }
   std::vector<double*> peers(static_cast<size_t>(nranks), nullptr);

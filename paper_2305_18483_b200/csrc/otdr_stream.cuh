@@ -88,10 +88,32 @@ __device__ __forceinline__ unsigned long long* xflag(double* buf, int par, int s
 }
 // publish this rank's contribution of epoch e: caller has fenced its data
 // stores at system scope; one thread per CTA-group calls this.
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void xpublish(double* const* peers, int rank, int nranks, long long n,
                                          unsigned long long e) {
-  __threadfence_system();
-  for (int r = 0; r < nranks; ++r) st_release_sys(xflag(peers[r], int(e & 1), rank, nranks, n), e);
+  // one system-scope fence (cumulative over the CTA's and, through the grid
+  // barriers, the grid's prior peer stores), then relaxed flag stores
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  for (int r = 0; r < nranks; ++r) st_relaxed_sys(xflag(peers[r], int(e & 1), rank, nranks, n), e);
+}
+// Fixed-order fold of count values (stride apart) by one warp: every load is
+// issued before any add (one L2 round trip for count <= 32 * 16).
+__device__ __forceinline__ double warp_fold_strided(const double* p, int count, int stride) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int base = 0; base < count; base += 32 * 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = base + u * 32 + lane;
+      v[u] = i < count ? __ldcg(p + (long long)i * stride) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) s += v[u];
+  }
+  return warp_sum(s);
 }
 __device__ __forceinline__ void xwait(double* rbuf, int nranks, long long n, unsigned long long e) {
   for (int r = 0; r < nranks; ++r) {
@@ -361,7 +383,6 @@ __device__ __forceinline__ void stream_stripe_done(const StreamArgs& A, long lon
     for (int t = t0; t < t1; ++t) S += __ldcg(src + (long long)t * kStreamTN);
     if (A.peers) {  // local column sums to every rank's receive slot (NVLink stores)
       for (int r = 0; r < A.nranks; ++r) xslot(A.peers[r], par, A.rank, A.nranks, A.n)[j] = S;
-      __threadfence_system();
     } else {
       const double sj = __dsub_rn(S, A.q[j]);
       A.s[j] = sj;
@@ -369,7 +390,14 @@ __device__ __forceinline__ void stream_stripe_done(const StreamArgs& A, long lon
     }
   }
   if (A.peers) {
-    if (threadIdx.x == 0) A.scnt[stripe] = 0;
+    // one system-scope fence per completed stripe, after the CTA's stores
+    // (bar.sync orders them before thread 0's fence; the flag publish after
+    // the grid barriers is a release at system scope)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      A.scnt[stripe] = 0;
+    }
     return;
   }
   const double tot = block_sum(ss, sred);
@@ -412,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
 
   auto stamp = [&](int slot) {
     if (A.tstamp && it < kTraceIters && threadIdx.x == 0 && (slot < P ? true : c == 0))
-      A.tstamp[it * (P + 8) + slot] = globaltimer_ns();
+      A.tstamp[it * (P + 12) + slot] = globaltimer_ns();
   };
   for (;;) {
     stamp(P + 0);
@@ -476,21 +504,19 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
       // exchange: CTA 0 sends this rank's (sum r, sum r^2, sum R) and the
       // epoch flags; every CTA waits for all ranks, then folds in rank order
       if (c == 0 && warp < 3) {
-        double u = 0.0;
-        for (int cc = lane; cc < P; cc += 32) u += __ldcg(A.part + cc * 4 + warp);
-        u = warp_sum(u);
-        if (lane == 0) {
+        const double u = warp_fold_strided(A.part + warp, P, 4);
+        if (lane == 0)
           for (int r = 0; r < A.nranks; ++r)
             xslot(A.peers[r], int(epoch & 1), A.rank, A.nranks, n)[n + warp] = u;
-          __threadfence_system();
-        }
       }
       if (c == 0) {
         __syncthreads();
         if (threadIdx.x == 0) xpublish(A.peers, A.rank, A.nranks, n, epoch);
       }
+      stamp(P + 8);
       if (threadIdx.x == 0) xwait(A.rbuf, A.nranks, n, epoch);
       __syncthreads();
+      stamp(P + 9);
       if (warp < 3) {
         double u = 0.0;
         if (lane == 0)
@@ -519,23 +545,19 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
       }
       const double t4 = block_sum(ssq, sred);
       if (threadIdx.x == 0) A.part[c * 4 + 3] = t4;
+      stamp(P + 10);
       grid_barrier(&ctl->bar_str);  // phi / psi / s complete, ssq partials visible
+      stamp(P + 11);
       if (warp == 0) {
-        double u = 0.0;
-        for (int cc = lane; cc < P; cc += 32) u += __ldcg(A.part + cc * 4 + 3);
-        u = warp_sum(u);
+        const double u = warp_fold_strided(A.part + 3, P, 4);
         if (lane == 0) bc[3] = u;
       }
       __syncthreads();
     } else if (warp < 3) {
-      double u = 0.0;
-      for (int cc = lane; cc < P; cc += 32) u += __ldcg(A.part + cc * 4 + warp);
-      u = warp_sum(u);
+      const double u = warp_fold_strided(A.part + warp, P, 4);
       if (lane == 0) bc[warp] = u;
     } else if (warp == 3) {  // sum s^2: stripe partials in stripe order
-      double u = 0.0;
-      for (int t = lane; t < A.stripes; t += 32) u += __ldcg(A.sspart + t);
-      u = warp_sum(u);
+      const double u = warp_fold_strided(A.sspart, A.stripes, 1);
       if (lane == 0) bc[3] = u;
     }
     if (!peer) {
