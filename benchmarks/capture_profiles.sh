@@ -14,6 +14,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:stre
   -o gpurun_out/stream -f python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_stream.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 3 -c 1 \
   -o gpurun_out/sweep -f python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_sweep.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gl_ -s 3 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gl_pipe -s 3 -c 1 \
   -o gpurun_out/gl -f python benchmarks/variants.py cfg3 > gpurun_out/ncu_gl.log 2>&1
-echo done
+
+timeout 600 python benchmarks/configs.py cfg1 cfg2 cfg3 cfg4 cfg5 > gpurun_out/configs.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1
+echo all_done
