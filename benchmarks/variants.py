@@ -24,7 +24,8 @@ cfg = CFG
 if cfg in ("headline", "cfg2", "cfg4", "cfg1") or cfg.startswith("n"):
     m = {"headline": 20000, "cfg2": 10000, "cfg4": 40000, "cfg1": 1000}.get(cfg) or int(cfg[1:])
     reg = {"cfg2": otdr.ZeroReg()}.get(cfg, otdr.QuadraticReg(5e-3 * 2 * m))
-    eng = otdr.Engine(m, m, "f32")
+    st = os.environ.get("OTDRB_STORAGE", "f32")
+    eng = otdr.Engine(m, m, st)
     src, tgt = datagen.gaussian_points(m, m, 0)
     eng.build_sqdist_cost(src, tgt, datagen.uniform(m), datagen.uniform(m))
 else:
@@ -39,7 +40,7 @@ rho = otdr.default_stepsize(m, m)
 eng.step(rho, 5)
 ms = eng.time_steps(rho, ITERS) / ITERS
 prof = eng.profile(rho, 5)
-alg = 12.0 * m * m
+alg = (24.0 if os.environ.get("OTDRB_STORAGE") == "f64" else 12.0) * m * m
 print("RESULT " + json.dumps(dict(cfg=cfg, variant=VARIANT, path=eng.solve_path(), ms_per_iter=ms, iters_per_s=1e3 / ms,
       sweep_ms=prof["sweep_ms"], sweep_GBps=alg / prof["sweep_ms"] / 1e6,
       iter_GBps=alg / ms / 1e6, prof=prof)), flush=True)

@@ -139,7 +139,7 @@ struct otdr_dev {
   bool allow_stream = true;
   int str_P = 0, str_ntiles = 0, str_tpc = 8, str_tail = 4;
   double *str_part = nullptr, *str_colpart = nullptr;
-  int4* d_tiles = nullptr;
+  int str_big = 1, str_small = 1, str_head = 0;
   int* d_sfirst = nullptr;
   unsigned* d_scnt = nullptr;
   double* str_sspart = nullptr;
@@ -700,28 +700,28 @@ struct otdr_dev {
     const long long small = std::min(big, std::max<long long>(std::min<long long>(96, min_rows), big / std::max(1, str_tail)));
     const long long tail_stripes =
         str_tail > 1 ? std::min<long long>(S, (P * big + m_loc - 1) / m_loc) : 0;
-    std::vector<int4> tiles;
     std::vector<int> first;
+    long long ntiles = 0;
     for (long long st = 0; st < S; ++st) {
-      first.push_back(int(tiles.size()));
+      first.push_back(int(ntiles));
       const long long R = st >= S - tail_stripes ? small : big;
-      for (long long r0 = 0; r0 < m_loc; r0 += R)
-        tiles.push_back(int4{int(st), int(r0), int(std::min(m_loc, r0 + R)), 0});
+      ntiles += (m_loc + R - 1) / R;
     }
-    first.push_back(int(tiles.size()));
-    for (void* ptr : {(void*)str_part, (void*)str_colpart, (void*)d_tiles, (void*)d_sfirst,
+    first.push_back(int(ntiles));
+    str_big = int(big);
+    str_small = int(small);
+    str_head = int(S - tail_stripes);
+    for (void* ptr : {(void*)str_part, (void*)str_colpart, (void*)d_sfirst,
                       (void*)d_scnt, (void*)str_sspart})
       if (ptr) cudaFree(ptr);
     d_scnt = dalloc<unsigned>(size_t(S));
     CK(cudaMemset(d_scnt, 0, size_t(S) * sizeof(unsigned)));
     str_sspart = dalloc<double>(size_t(S));
     str_part = dalloc<double>(size_t(P) * 4);
-    str_colpart = dalloc<double>(tiles.size() * otdrk::kStreamTN);
-    d_tiles = dalloc<int4>(tiles.size());
+    str_colpart = dalloc<double>(size_t(ntiles) * otdrk::kStreamTN);
     d_sfirst = dalloc<int>(first.size());
-    CK(cudaMemcpy(d_tiles, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_sfirst, first.data(), first.size() * sizeof(int), cudaMemcpyHostToDevice));
-    str_ntiles = int(tiles.size());
+    str_ntiles = int(ntiles);
     str_P = int(P);
   }
 
@@ -773,7 +773,9 @@ struct otdr_dev {
 
   void launch_stream(long long iters) {
     const long long S = (ld + otdrk::kStreamTN - 1) / otdrk::kStreamTN;
-    otdrk::StreamArgs sa{X, C, phi, a, r, p, psi, b, s, q, rowpart, str_colpart, d_tiles,
+    const int nb = int((m_loc + str_big - 1) / str_big), ns = int((m_loc + str_small - 1) / str_small);
+    otdrk::StreamArgs sa{X, C, phi, a, r, p, psi, b, s, q, rowpart, str_colpart,
+                         str_big, str_small, str_head, nb, ns,
                          d_sfirst, d_scnt, str_sspart, str_part, d_ctl, d_prm, m_loc, n, ld, int(S), str_ntiles,
                          iters, nullptr, m_glob, sharded ? d_peers : nullptr, rbuf, d_xep,
                          cfg.rank, cfg.nranks};
@@ -1181,7 +1183,7 @@ struct otdr_dev {
   void release() {
     invalidate_graphs();
     void* ptrs[] = {C, X, p, q, phi, psi, a, b, r, s, rowpart, colpart, exch, bpart, cpart,
-                    str_part, str_colpart, d_tiles, d_sfirst, d_scnt, str_sspart, d_glp_pos,
+                    str_part, str_colpart, d_sfirst, d_scnt, str_sspart, d_glp_pos,
                     csum, stage, fpart, fpart2, gscratch, d_dev_row, d_seg, d_cert_seg, d_prm, d_ctl, d_trace, d_mx};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);

@@ -49,7 +49,9 @@ struct StreamArgs {
   const double* q;
   double* rowpart;        // [m][stripes]
   double* colpart;        // [ntiles][TN] one slot per tile
-  const int4* tiles;      // [ntiles] {stripe, row begin, row end, -}, stripe-major
+  // tiles, stripe-major: the first `head` stripes in row runs of `big`, the
+  // rest in runs of `small` (tile id -> stripe / rows is arithmetic, no load)
+  int big, small, head, nb, ns;
   const int* sfirst;      // [stripes + 1] first tile of each stripe
   unsigned* scnt;         // [stripes] tiles completed this sweep (zero between sweeps)
   double* sspart;         // [stripes] sum of s_j^2 over the stripe's columns
@@ -450,7 +452,26 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
       __syncthreads();
       const int tile = (int)s_tile;  // the tile sweep ends with __syncthreads
       if (tile >= A.ntiles) break;
-      const int4 tl = A.tiles[tile];
+      int4 tl;
+      {
+        const int hb = A.head * A.nb;
+        int st_, k_, R_;
+        if (tile < hb) {
+          st_ = tile / A.nb;
+          k_ = tile - st_ * A.nb;
+          R_ = A.big;
+        } else {
+          const int t2 = tile - hb;
+          const int q2 = t2 / A.ns;
+          st_ = A.head + q2;
+          k_ = t2 - q2 * A.ns;
+          R_ = A.small;
+        }
+        const long long r0_ = (long long)k_ * R_;
+        tl.x = st_;
+        tl.y = (int)r0_;
+        tl.z = (int)((r0_ + R_ < m) ? r0_ + R_ : m);
+      }
       if constexpr (D > 0) {
         stream_segment_async<T, REG, EXACT, NV, D>(A, tile, tl.x, tl.y, tl.z, rho, qd, qinv, red, squeue);
       } else {
