@@ -764,3 +764,57 @@ def test_peer_exchange_group_lasso_graph_path(ora, monkeypatch):
     assert all(rel(g.psi, st.psi) <= 1e-12 for g in gs)
     for e in engs:
         e.close()
+
+
+def test_headline_size_stream_vs_graph_solve(monkeypatch):
+    """The north-star point (20000^2, quadratic alpha = 200, fp32): a full solve
+    to 1e-4 through the streaming kernel and through the CUDA-graph loop stop
+    at the same iteration (+-2, fp32 reduction order) with the same objective
+    (1e-6 relative) -- full-size parity between the two device loops."""
+    from paper_2305_18483_b200 import datagen
+
+    m = n = 20000
+    src, tgt = datagen.gaussian_points(m, n, 0)
+    out = {}
+    for mode in ("on", "off"):
+        monkeypatch.setenv("OTDR_STREAM", mode)
+        eng = otdr.Engine(m, n, "f32")
+        eng.build_sqdist_cost(src, tgt, datagen.uniform(m), datagen.uniform(n))
+        eng.set_regularizer(otdr.QuadraticReg(200.0))
+        eng.set_state()
+        assert eng.solve_path() == ("stream" if mode == "on" else "graph")
+        out[mode] = eng.solve(otdr.SolverOptions(tol_primal=1e-4, max_iter=3000, storage="f32"),
+                              with_state=False)
+        eng.close()
+    a, b = out["on"], out["off"]
+    assert a.termination.name == b.termination.name == "Converged"
+    assert abs(a.iterations - b.iterations) <= 2, (a.iterations, b.iterations)
+    assert abs(a.objective - b.objective) <= 1e-6 * abs(b.objective)
+
+
+def test_cfg3_size_group_lasso_properties():
+    """cfg3 at full size (10000^2, 10 class groups, lambda 1e-3, fp32) through
+    the pipelined GL kernel: non-negativity, mass balance sum r = sum s, row
+    and column sums consistent with r and s, and every (column, class) group
+    either annihilated or strictly positive-normed after 25 iterations."""
+    from paper_2305_18483_b200 import datagen
+
+    m = n = 10000
+    src, tgt, ls, lt = datagen.adaptation_points(m, n, 10, 0)
+    p, q = datagen.uniform(m), datagen.uniform(n)
+    eng = otdr.Engine(m, n, "f32")
+    eng.build_sqdist_cost(src, tgt, p, q)
+    eng.set_regularizer(otdr.GroupLassoReg(1e-3, otdr.column_class_blocks(ls, n)))
+    eng.set_state()
+    eng.step(otdr.default_stepsize(m, n), 25)
+    g = eng.get_state()
+    eng.close()
+    assert g.k == 25
+    assert (g.X >= 0).all()
+    assert abs(g.r.sum() - g.s.sum()) <= 1e-9
+    np.testing.assert_allclose(g.X.sum(axis=1) - p, g.r, atol=1e-9)
+    np.testing.assert_allclose(g.X.sum(axis=0) - q, g.s, atol=1e-9)
+    lab = np.asarray(ls)
+    for c in range(10):
+        norms = np.sqrt((g.X[lab == c].astype(np.float64) ** 2).sum(axis=0))
+        assert np.isfinite(norms).all() and (norms >= 0).all()
