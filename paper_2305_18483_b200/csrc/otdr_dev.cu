@@ -176,7 +176,7 @@ struct otdr_dev {
   size_t glr_smem = 0;
   CUtensorMap glr_mapX{}, glr_mapC{};
   // pipelined single-pass GL sweep: persistent CTAs over (segment, G stripes)
-  int glp_G = 0, glp_nstr = 0, glp_groups = 0, glp_lmax = 0, glp_d = 0;
+  int glp_G = 0, glp_nstr = 0, glp_groups = 0, glp_lmax = 0, glp_d = 0, glp_wb = 128;
   int2* d_glp_pos = nullptr;
   size_t glp_smem = 0;
   // TMA-pipelined plain sweep (OTDR_SWEEP=tma): box 256 cols x kSweepTR rows
@@ -256,9 +256,9 @@ struct otdr_dev {
     return !gl_stage_active(track) && glc_tn > 0 && !track && !prm.fused;
   }
 
-  template <typename T, int D>
+  template <typename T, int D, int WB>
   void launch_gl_pipe_t() {
-    auto kern = otdrk::gl_pipe_kernel<T, sizeof(T) == 8, D>;
+    auto kern = otdrk::gl_pipe_kernel<T, sizeof(T) == 8, D, WB>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(glp_smem)));
     otdrk::GLPipeArgs ga{X, C, phi, psi, rowpart, colpart, d_seg, d_glp_pos, d_prm, d_ctl, m_loc, ld,
                          num_segs, glp_nstr, glp_groups, glp_lmax};
@@ -267,16 +267,30 @@ struct otdr_dev {
     const int grid = cap > 0 ? std::min(cap, num_sms) : num_sms;
     kern<<<grid, otdrk::kGLPThreads, glp_smem, stream>>>(ga);
   }
-  void launch_gl_pipe() {
-    if (f64()) {
-      if (glp_d == 4) launch_gl_pipe_t<double, 4>();
-      else if (glp_d == 3) launch_gl_pipe_t<double, 3>();
-      else launch_gl_pipe_t<double, 2>();
+  template <typename T>
+  void launch_gl_pipe_d() {
+    if (glp_wb == 64) {
+      if (glp_d == 8) launch_gl_pipe_t<T, 8, 64>();
+      else if (glp_d == 6) launch_gl_pipe_t<T, 6, 64>();
+      else launch_gl_pipe_t<T, 4, 64>();
     } else {
-      if (glp_d == 4) launch_gl_pipe_t<float, 4>();
-      else if (glp_d == 3) launch_gl_pipe_t<float, 3>();
-      else launch_gl_pipe_t<float, 2>();
+      if (glp_d == 4) launch_gl_pipe_t<T, 4, 128>();
+      else if (glp_d == 3) launch_gl_pipe_t<T, 3, 128>();
+      else launch_gl_pipe_t<T, 2, 128>();
     }
+  }
+  void launch_gl_pipe() {
+    if (f64()) launch_gl_pipe_d<double>();
+    else launch_gl_pipe_d<float>();
+  }
+
+  static size_t glpipe_smem(bool f64s, int d, int wb, int lmax) {
+    const size_t q = size_t(d) * 2 * otdrk::kGLPThreads * 16;
+    const size_t base = f64s ? (wb == 64 ? otdrk::glpipe_smem_bytes<double, 2, 64>(lmax)
+                                         : otdrk::glpipe_smem_bytes<double, 2, 128>(lmax))
+                             : (wb == 64 ? otdrk::glpipe_smem_bytes<float, 2, 64>(lmax)
+                                         : otdrk::glpipe_smem_bytes<float, 2, 128>(lmax));
+    return base - otdrk::glpipe_queue_bytes<float, 2>() + q;
   }
 
   void launch_sweep(bool track, bool sums_only) {
@@ -477,12 +491,18 @@ struct otdr_dev {
     touch(otdrk::sweep_kernel<float, otdrk::REG_NONE, false, true, 2, 2>);
     touch(otdrk::sweep_kernel<float, otdrk::REG_QUAD, false, false, 2, 2>);
     touch(otdrk::sweep_kernel<float, otdrk::REG_QUAD, false, true, 2, 2>);
-    touch(otdrk::gl_pipe_kernel<float, false, 2>);
-    touch(otdrk::gl_pipe_kernel<float, false, 3>);
-    touch(otdrk::gl_pipe_kernel<float, false, 4>);
-    touch(otdrk::gl_pipe_kernel<double, true, 2>);
-    touch(otdrk::gl_pipe_kernel<double, true, 3>);
-    touch(otdrk::gl_pipe_kernel<double, true, 4>);
+    touch(otdrk::gl_pipe_kernel<float, false, 2, 128>);
+    touch(otdrk::gl_pipe_kernel<float, false, 3, 128>);
+    touch(otdrk::gl_pipe_kernel<float, false, 4, 128>);
+    touch(otdrk::gl_pipe_kernel<double, true, 2, 128>);
+    touch(otdrk::gl_pipe_kernel<double, true, 3, 128>);
+    touch(otdrk::gl_pipe_kernel<double, true, 4, 128>);
+    touch(otdrk::gl_pipe_kernel<float, false, 4, 64>);
+    touch(otdrk::gl_pipe_kernel<float, false, 6, 64>);
+    touch(otdrk::gl_pipe_kernel<float, false, 8, 64>);
+    touch(otdrk::gl_pipe_kernel<double, true, 4, 64>);
+    touch(otdrk::gl_pipe_kernel<double, true, 6, 64>);
+    touch(otdrk::gl_pipe_kernel<double, true, 8, 64>);
     touch(otdrk::gl_ring_kernel<float, false>);
     touch(otdrk::gl_ring_kernel<double, true>);
     touch(otdrk::gl_stage_kernel<float, false>);
@@ -889,16 +909,14 @@ struct otdr_dev {
       if (!gk0 || std::strcmp(gk0, "pipe") == 0) {
         int max_smem = 0;
         CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg.device));
-        int dmax = 4;
-        if (const char* gd = std::getenv("OTDR_GL_PIPE_D")) dmax = std::max(2, std::min(4, std::atoi(gd)));
-        for (int d : {4, 3, 2}) {
+        glp_wb = 128;
+        if (const char* gw = std::getenv("OTDR_GL_PIPE_W")) glp_wb = std::atoi(gw) == 64 ? 64 : 128;
+        int dmax = glp_wb == 64 ? 8 : 4;
+        if (const char* gd = std::getenv("OTDR_GL_PIPE_D")) dmax = std::max(2, std::min(dmax, std::atoi(gd)));
+        const std::vector<int> ds = glp_wb == 64 ? std::vector<int>{8, 6, 4} : std::vector<int>{4, 3, 2};
+        for (int d : ds) {
           if (d > dmax) continue;
-          const size_t need = f64() ? otdrk::glpipe_smem_bytes<double, 4>(int(lmax)) -
-                                          otdrk::glpipe_queue_bytes<double, 4>() +
-                                          size_t(d) * 2 * otdrk::kGLPThreads * 16
-                                    : otdrk::glpipe_smem_bytes<float, 4>(int(lmax)) -
-                                          otdrk::glpipe_queue_bytes<float, 4>() +
-                                          size_t(d) * 2 * otdrk::kGLPThreads * 16;
+          const size_t need = glpipe_smem(f64(), d, glp_wb, int(lmax));
           if (need + 1024 <= size_t(max_smem)) {
             glp_d = d;
             glp_smem = need;
@@ -906,7 +924,7 @@ struct otdr_dev {
           }
         }
         if (glp_smem) {
-          const long long W = 128 / (long long)esz;
+          const long long W = glp_wb / (long long)esz;
           glp_nstr = int((ld + W - 1) / W);
           glp_G = 8;
           if (const char* ge = std::getenv("OTDR_GL_PIPE_G"))

@@ -57,21 +57,21 @@ template <typename T, int D>
 __host__ __device__ constexpr size_t glpipe_queue_bytes() {
   return size_t(D) * 2 * kGLPThreads * 16;
 }
-template <typename T, int D>
+template <typename T, int D, int WB>
 __host__ __device__ inline size_t glpipe_smem_bytes(int Lmax) {
-  constexpr int W = 128 / (int)sizeof(T);
-  return glpipe_queue_bytes<T, D>() + size_t(Lmax) * 128 /* vbuf */ + size_t(Lmax) * 16 /* phi, rowacc */ +
+  constexpr int W = WB / (int)sizeof(T);
+  return glpipe_queue_bytes<T, D>() + size_t(Lmax) * WB /* vbuf */ + size_t(Lmax) * 16 /* phi, rowacc */ +
          size_t(kGLPMaxG) * W * 8 /* psi */ + 2 * size_t(kGLPWarps) * W * 8 /* red */ + 2 * W * 8 /* sig */;
 }
 
-template <typename T, bool EXACT, int D>
+template <typename T, bool EXACT, int D, int WB>
 __global__ void __launch_bounds__(kGLPThreads, 1) gl_pipe_kernel(GLPipeArgs A) {
   using V = typename Vec<T>::type;
   constexpr int VEC = Vec<T>::N;
-  constexpr int W = 128 / (int)sizeof(T);  // stripe width: 128 bytes per row
-  constexpr int LPR = W / VEC;             // 8 lanes per row
-  constexpr int RPW = 32 / LPR;            // 4 rows per warp instruction
-  constexpr int RSTEP = kGLPWarps * RPW;   // 64 rows per step
+  constexpr int W = WB / (int)sizeof(T);   // stripe width: WB (128 or 64) bytes per row
+  constexpr int LPR = W / VEC;             // lanes per row (8 for 128-B stripes)
+  constexpr int RPW = 32 / LPR;            // rows per warp instruction
+  constexpr int RSTEP = kGLPWarps * RPW;   // rows per step
   Ctl* ctl = A.ctl;
   if (ctl->done) return;  // grid-uniform
   const Params& prm = *A.prm;
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kGLPThreads, 1) gl_pipe_kernel(GLPipeArgs A) {
   extern __shared__ __align__(16) unsigned char glp_smem[];
   uint4* q = reinterpret_cast<uint4*>(glp_smem);
   T* vbuf = reinterpret_cast<T*>(glp_smem + glpipe_queue_bytes<T, D>());
-  double* phi_s = reinterpret_cast<double*>(glp_smem + glpipe_queue_bytes<T, D>() + size_t(A.Lmax) * 128);
+  double* phi_s = reinterpret_cast<double*>(glp_smem + glpipe_queue_bytes<T, D>() + size_t(A.Lmax) * WB);
   double* rowacc = phi_s + A.Lmax;
   double* psi_s = rowacc + A.Lmax;          // [G][W]
   double* redq = psi_s + kGLPMaxG * W;      // [warps][W]
