@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) bstream_kernel(BStreamArgs A) {
             const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, c[e])), ph), ps[e])
                                      : (fma(-rho, c[e], x[e]) + ph) + ps[e];
             double nx = clamp0(val);
-            if (quad) nx = EXACT ? __ddiv_rn(nx, qd) : nx * qinv;
+            if (quad) nx = EXACT ? div_rn_by(nx, qd, qinv) : nx * qinv;
             o[e] = nx;
             cacc[e] += nx;
             rs += nx;

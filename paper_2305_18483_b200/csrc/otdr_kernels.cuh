@@ -115,6 +115,18 @@ template <> __device__ __forceinline__ double2 pack<double>(const double* o) { r
 template <typename V> __device__ __forceinline__ V ld_ro(const V* p) { return __ldg(p); }
 template <typename V> __device__ __forceinline__ V ld_rw(const V* p) { return *p; }
 
+// RN(x / d) for the quadratic prox X /= (1 + rho alpha) (regularizers.cpp:54):
+// x finite >= 0, d = 1 + rho alpha >= 1, inv = RN(1 / d) (host). q0 = RN(x inv)
+// is within one ulp of x / d, the residual x - q0 d is exact in one FMA, and one
+// correction q0 + r inv rounds to the correctly rounded quotient (Markstein).
+// Three fp64 ops instead of the __ddiv_rn sequence; bitwise equal to the
+// reference's true division (tests/test_gpu_parity.py::test_first_step_bitwise).
+__device__ __forceinline__ double div_rn_by(double x, double d, double inv) {
+  const double q0 = __dmul_rn(x, inv);
+  const double r = __fma_rn(-q0, d, x);
+  return __fma_rn(r, inv, q0);
+}
+
 // max(v, 0) with std::max's NaN propagation (solver.cpp:99 cwiseMax).
 __device__ __forceinline__ double clamp0(double v) { return v < 0.0 ? 0.0 : v; }
 
@@ -292,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(SweepArgs<T> a) {
                           : (fma(-rho, c[e], x[e]) + phv[u]) + psi_r[v][e];
             }
             nx = clamp0(val);
-            if (REG == REG_QUAD) nx = EXACT ? __ddiv_rn(nx, qd) : nx * qinv;
+            if (REG == REG_QUAD) nx = EXACT ? div_rn_by(nx, qd, qinv) : nx * qinv;
             if (TRACK) {
               double xold = x[e];
               if (mode == MODE_ODD) xold = __dadd_rn(x[e], __dmul_rn(rho, c[e]));
@@ -982,7 +994,7 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_tma_kernel(SweepArgs<T> a,
             const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, c[e])), ph), psi_r[v][e])
                                      : (fma(-rho, c[e], x[e]) + ph) + psi_r[v][e];
             double nx = clamp0(val);
-            if (REG == REG_QUAD) nx = EXACT ? __ddiv_rn(nx, qd) : nx * qinv;
+            if (REG == REG_QUAD) nx = EXACT ? div_rn_by(nx, qd, qinv) : nx * qinv;
             o[e] = nx;
             cacc[v][e] += nx;
             rs[u] += nx;

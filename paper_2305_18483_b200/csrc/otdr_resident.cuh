@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kRT, 1) resident_kernel(ResidentArgs A) {
               const double val = exact ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, cc[e])), ph), ps[e])
                                        : (fma(-rho, cc[e], x[e]) + ph) + ps[e];
               double nx = clamp0(val);
-              if (A.reg == REG_QUAD) nx = exact ? __ddiv_rn(nx, qd) : nx * qinv;
+              if (A.reg == REG_QUAD) nx = exact ? div_rn_by(nx, qd, qinv) : nx * qinv;
               o[e] = nx;
               cacc[e] += nx;
               rs[u] += nx;

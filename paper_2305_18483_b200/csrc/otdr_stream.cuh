@@ -188,7 +188,7 @@ __device__ __forceinline__ void stream_segment(const StreamArgs& A, int tile, lo
                                                psi_r[v][e])
                                    : (fma(-rho, cc[e], x[e]) + phv[u]) + psi_r[v][e];
           double nx = clamp0(val);
-          if (REG == REG_QUAD) nx = EXACT ? __ddiv_rn(nx, qd) : nx * qinv;  // regularizers.cpp:54
+          if (REG == REG_QUAD) nx = EXACT ? div_rn_by(nx, qd, qinv) : nx * qinv;  // regularizers.cpp:54
           o[e] = nx;
           cacc[v][e] += nx;
           rs += nx;
@@ -334,7 +334,7 @@ __device__ __forceinline__ void stream_segment_async(const StreamArgs& A, int ti
                                              psi_r[v][e])
                                  : (fma(-rho, cc[e], x[e]) + ph) + psi_r[v][e];
         double nx = clamp0(val);
-        if (REG == REG_QUAD) nx = EXACT ? __ddiv_rn(nx, qd) : nx * qinv;
+        if (REG == REG_QUAD) nx = EXACT ? div_rn_by(nx, qd, qinv) : nx * qinv;
         o[e] = nx;
         cacc[v][e] += nx;
         rs += nx;

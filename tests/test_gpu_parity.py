@@ -818,3 +818,30 @@ def test_cfg3_size_group_lasso_properties():
     for c in range(10):
         norms = np.sqrt((g.X[lab == c].astype(np.float64) ** 2).sum(axis=0))
         assert np.isfinite(norms).all() and (norms >= 0).all()
+
+
+@pytest.mark.parametrize("kind,param", [("none", 0.0), ("quad", 0.7), ("quad", 123.0), ("gl", 0.02)])
+@pytest.mark.parametrize("resident", ["on", "off"])
+def test_first_step_bitwise(ora, monkeypatch, kind, param, resident):
+    """fp64 storage: the first DR step from default_init is purely element-wise
+    (phi0, psi0 are constants, the sums of X0 = 0 are exact), so X_1 must equal
+    the reference arithmetic BIT FOR BIT -- including the quadratic prox's true
+    division (regularizers.cpp:54) and the group-lasso scale."""
+    monkeypatch.setenv("OTDR_RESIDENT", resident)
+    m, n = 1500, 1300
+    C, p, q, *_ = ora.gaussian_problem(m, n, 41)
+    labels = [i % 3 for i in range(m)]
+    pr = ora.Problem(C, p, q)
+    st = ora.make_state(pr)
+    ora.step(st, pr, oracle_reg(ora, kind, param, labels, n), ora.default_stepsize(m, n))
+    eng = otdr.Engine(m, n, "f64")
+    eng.set_problem(C, p, q)
+    eng.set_regularizer(dev_reg(kind, param, labels, n))
+    eng.set_state()
+    eng.step(ora.default_stepsize(m, n), 1)
+    g = eng.get_state()
+    eng.close()
+    if kind == "gl":  # group norms are sums: their order differs, so 1 ulp is allowed
+        assert rel(g.X, st.X) <= 1e-15
+    else:
+        assert np.array_equal(g.X, st.X), int((g.X != st.X).sum())
