@@ -147,10 +147,12 @@ __global__ void __launch_bounds__(kGLPThreads, 1) gl_pipe_kernel(GLPipeArgs A) {
       const long long col2 = col1 - W;                                   // phase-2 columns
       const bool ok1 = ph1 && col1 < A.ld, ok2 = ph2 && col2 < A.ld;
       double ps[VEC], sc[VEC], sq[VEC];
+      float sc32[VEC];
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
         ps[e] = ph1 ? psi_s[j * W + sub * VEC + e] : 0.0;
         sc[e] = ph2 ? sig[((j - 1) & 1) * W + sub * VEC + e] : 0.0;
+        sc32[e] = (float)sc[e];
         sq[e] = 0.0;
         cs[e] = 0.0;
       }
@@ -161,16 +163,31 @@ __global__ void __launch_bounds__(kGLPThreads, 1) gl_pipe_kernel(GLPipeArgs A) {
         if (ph2) {  // stripe j-1: X = v * sigma, sums
           double rs = 0.0;
           if (valid && ok2) {
-            double v[VEC], o[VEC];
-            unpack(*reinterpret_cast<const V*>(vrow), v);
+            if constexpr (EXACT) {
+              double v[VEC], o[VEC];
+              unpack(*reinterpret_cast<const V*>(vrow), v);
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-              const double nx = sg.grouped ? (EXACT ? __dmul_rn(v[e], sc[e]) : v[e] * sc[e]) : v[e];
-              o[e] = nx;
-              cs[e] += nx;
-              rs += nx;
+              for (int e = 0; e < VEC; ++e) {
+                const double nx = sg.grouped ? __dmul_rn(v[e], sc[e]) : v[e];
+                o[e] = nx;
+                cs[e] += nx;
+                rs += nx;
+              }
+              *reinterpret_cast<V*>(X + (sg.begin + r) * A.ld + col2) = pack<T>(o);
+            } else {
+              // fp32 storage: the staged v is fp32 already, scale in fp32 (<= 1
+              // ulp from rounding v * sigma in fp64) and widen once for the sums
+              V vv = *reinterpret_cast<const V*>(vrow);
+              float* vf = reinterpret_cast<float*>(&vv);
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) {
+                if (sg.grouped) vf[e] = __fmul_rn(vf[e], sc32[e]);
+                const double nx = vf[e];
+                cs[e] += nx;
+                rs += nx;
+              }
+              *reinterpret_cast<V*>(X + (sg.begin + r) * A.ld + col2) = vv;
             }
-            *reinterpret_cast<V*>(X + (sg.begin + r) * A.ld + col2) = pack<T>(o);
           }
 #pragma unroll
           for (int o = 1; o < LPR; o <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
