@@ -42,7 +42,7 @@ struct otdr_batch {
   bool use_stream = false;
   int bs_nch = 0, bs_nsets = 0;
   size_t bs_smem = 0;
-  static constexpr int kBSD = 3;
+  static constexpr int kBSD = 6;
   int bs_nt = 512;  // threads per problem CTA (OTDR_BATCH_THREADS=256: two CTAs per SM)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
