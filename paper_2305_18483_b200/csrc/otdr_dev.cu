@@ -434,12 +434,12 @@ struct otdr_dev {
     otdrk::reduce_kernel<<<RB + CB, otdrk::kThreads, 0, stream>>>(ra);
   }
 
-  void launch_exchange(double* buf, size_t count) {
+  void launch_exchange(double* buf, size_t count, bool op_max = false) {
     if (comm) {
-      NK(nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, comm, stream));
+      NK(nccl().AllReduce(buf, buf, count, ncclDouble, op_max ? ncclMax : ncclSum, comm, stream));
     } else if (p2p) {
       otdrk::p2p_allreduce_kernel<<<1, 512, 0, stream>>>(buf, (long long)count, d_peers, rbuf, d_xep,
-                                                          cfg.rank, cfg.nranks, n);
+                                                          cfg.rank, cfg.nranks, n, op_max ? 1 : 0);
     } else if (cfg.nranks > 1) {
       throw Error{OTDR_E_STATE, "row-sharded context has no exchange: pass an NCCL id or link peers"};
     }
@@ -595,7 +595,7 @@ struct otdr_dev {
   // shards) reduce, all-reduce of the exchange vector, update; [certificate].
   void launch_iteration(bool track, bool cert, cudaGraphConditionalHandle cond, int use_cond) {
     launch_sweep(track, false);
-    if (comm == nullptr && use_fused_finalize) {
+    if (!sharded && use_fused_finalize) {
       launch_finalize(track, cond, use_cond, cert ? 1 : 0);
     } else {
       launch_reduce(false, track);
@@ -1492,15 +1492,18 @@ otdr_status otdr_dev_build_sqdist_cost(otdr_dev* ctx, const double* src_pts,
       otdrk::sqdist_kernel<float><<<grid, 256, 0, ctx->stream>>>((float*)ctx->C, d_src, d_tgt, d, ctx->m_loc, ctx->n, ctx->ld, d_mxv, ctx->d_mx, 0);
     ctx->check_launch();
     CK(cudaMemcpyAsync(d_mxv, ctx->d_mx, 8, cudaMemcpyDeviceToDevice, ctx->stream));
-    if (ctx->comm) NK(nccl().AllReduce(d_mxv, d_mxv, 1, ncclDouble, ncclMax, ctx->comm, ctx->stream));
+    if (ctx->sharded) ctx->launch_exchange(d_mxv, 1, /*op_max=*/true);  // global max (normalize_cost)
     if (ctx->f64())
       otdrk::sqdist_kernel<double><<<grid, 256, 0, ctx->stream>>>((double*)ctx->C, d_src, d_tgt, d, ctx->m_loc, ctx->n, ctx->ld, d_mxv, ctx->d_mx, 1);
     else
       otdrk::sqdist_kernel<float><<<grid, 256, 0, ctx->stream>>>((float*)ctx->C, d_src, d_tgt, d, ctx->m_loc, ctx->n, ctx->ld, d_mxv, ctx->d_mx, 1);
     ctx->check_launch();
     double mx = 0.0;
-    CK(cudaMemcpyAsync(&mx, d_mxv, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    // drain the stream (incl. the max exchange) before the pageable read-back:
+    // a pageable copy queued behind a spinning exchange kernel can hold the
+    // driver while the other ranks of this process still need to launch
     CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(&mx, d_mxv, 8, cudaMemcpyDeviceToHost));
     cudaFree(d_src);
     cudaFree(d_tgt);
     cudaFree(d_mxv);

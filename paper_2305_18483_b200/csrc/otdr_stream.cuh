@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
   }
 }
 
-// Small all-reduce (sum) of `count` <= n + 4 doubles over peer memory, for the
+// Small all-reduce (sum, or max when op_max) of `count` <= n + 4 doubles over peer memory, for the
 // non-hot exchanges of row-sharded runs (make_state sums, certificate / objective
 // partials, the group-lasso graph path): one CTA writes the vector into every
 // rank's receive slot, publishes the epoch flag, waits for every rank and sums
@@ -660,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
 __global__ void __launch_bounds__(512) p2p_allreduce_kernel(double* buf, long long count,
                                                              double* const* peers, double* rbuf,
                                                              unsigned long long* xep, int rank,
-                                                             int nranks, long long n) {
+                                                             int nranks, long long n, int op_max) {
   const unsigned long long e = *xep + 1;
   const int par = int(e & 1);
   for (long long t = threadIdx.x; t < count; t += blockDim.x) {
@@ -675,8 +675,11 @@ __global__ void __launch_bounds__(512) p2p_allreduce_kernel(double* buf, long lo
   }
   __syncthreads();
   for (long long t = threadIdx.x; t < count; t += blockDim.x) {
-    double s = 0.0;
-    for (int r = 0; r < nranks; ++r) s += __ldcg(xslot(rbuf, par, r, nranks, n) + t);
+    double s = op_max ? __ldcg(xslot(rbuf, par, 0, nranks, n) + t) : 0.0;
+    for (int r = op_max ? 1 : 0; r < nranks; ++r) {
+      const double v = __ldcg(xslot(rbuf, par, r, nranks, n) + t);
+      s = op_max ? (v > s ? v : s) : s + v;
+    }
     buf[t] = s;
   }
   __syncthreads();

@@ -845,3 +845,36 @@ def test_first_step_bitwise(ora, monkeypatch, kind, param, resident):
         assert rel(g.X, st.X) <= 1e-15
     else:
         assert np.array_equal(g.X, st.X), int((g.X != st.X).sum())
+
+
+def test_peer_exchange_device_cost_builder(ora, monkeypatch):
+    """Row-sharded device cost builder without NCCL: the normalising maximum
+    of squared_distance_cost (problem.cpp:68-74) is all-reduced (max) over
+    the peer buffers, so every rank's band equals the unsharded cost."""
+    monkeypatch.setenv("OTDR_STREAM_GRID", "100")
+    from paper_2305_18483_b200 import datagen, sharding
+
+    m, n = 700, 650
+    src, tgt = datagen.gaussian_points(m, n, 9)
+    p, q = datagen.uniform(m), datagen.uniform(n)
+    full = otdr.Engine(m, n, "f64")
+    full.build_sqdist_cost(src, tgt, p, q)
+    full.set_regularizer(otdr.QuadraticReg(1.0))
+    full.set_state()
+    full.step(otdr.default_stepsize(m, n), 6)
+    ref = full.get_state()
+    full.close()
+    bands = sharding.row_bands(m, 2)
+    engs = [otdr.Engine(m, n, "f64", shard=otdr.Shard(r, 2, lo, hi, None)) for r, (lo, hi) in enumerate(bands)]
+    otdr.link_local(engs)
+    _parallel([lambda e=e, lo=lo, hi=hi: e.build_sqdist_cost(src[lo:hi], tgt, p[lo:hi], q)
+               for e, (lo, hi) in zip(engs, bands)])
+    for e in engs:
+        e.set_regularizer(otdr.QuadraticReg(1.0))
+    _parallel([e.set_state for e in engs])
+    _parallel([lambda e=e: e.step(otdr.default_stepsize(m, n), 6) for e in engs])
+    gs = _parallel([e.get_state for e in engs])
+    X = np.concatenate([g.X for g in gs])
+    assert rel(X, ref.X) <= 1e-12, rel(X, ref.X)
+    for e in engs:
+        e.close()
