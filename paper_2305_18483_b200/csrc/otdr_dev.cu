@@ -138,6 +138,7 @@ struct otdr_dev {
   // persistent streaming solve (single GPU, zero / quadratic, HBM-resident plan)
   bool allow_stream = true;
   int str_P = 0, str_ntiles = 0, str_tpc = 8, str_tail = 4;
+  size_t str_part_cap = 0;
   double *str_part = nullptr, *str_colpart = nullptr;
   int str_big = 1, str_small = 1, str_head = 0;
   int* d_sfirst = nullptr;
@@ -282,6 +283,52 @@ struct otdr_dev {
   void launch_gl_pipe() {
     if (f64()) launch_gl_pipe_d<double>();
     else launch_gl_pipe_d<float>();
+  }
+
+  // Persistent group-lasso solve (one cooperative launch; OTDR_GL_STREAM=off
+  // keeps the CUDA-graph loop of gl_pipe + reduce + update).
+  bool allow_gl_stream = true;
+  bool gl_stream_active(bool track, bool cert) const {
+    return allow_gl_stream && reg_kind == OTDR_REG_GROUP_LASSO && gl_pipe_active(track) && !cert &&
+           (!sharded || p2p) && gls_grid > 0;
+  }
+  int gls_grid = 0;
+  template <typename T, int D, int WB>
+  void launch_gl_stream_t(long long iters) {
+    auto kern = otdrk::gl_stream_kernel<T, sizeof(T) == 8, D, WB>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(glp_smem)));
+    otdrk::GLStreamArgs ga{
+        otdrk::GLPipeArgs{X, C, phi, psi, rowpart, colpart, d_seg, d_glp_pos, d_prm, d_ctl, m_loc, ld,
+                          num_segs, glp_nstr, glp_groups, glp_lmax},
+        phi, psi, a, b, r, s, p, q, str_part, m_glob, n, sharded ? d_peers : nullptr, rbuf, d_xep,
+        cfg.rank, cfg.nranks, iters};
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(unsigned(gls_grid), 1, 1);
+    lc.blockDim = dim3(otdrk::kGLPThreads, 1, 1);
+    lc.dynamicSmemBytes = glp_smem;
+    lc.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, kern, ga));
+  }
+  template <typename T>
+  void launch_gl_stream_d(long long iters) {
+    if (glp_wb == 64) {
+      if (glp_d == 8) launch_gl_stream_t<T, 8, 64>(iters);
+      else if (glp_d == 6) launch_gl_stream_t<T, 6, 64>(iters);
+      else launch_gl_stream_t<T, 4, 64>(iters);
+    } else {
+      if (glp_d == 4) launch_gl_stream_t<T, 4, 128>(iters);
+      else if (glp_d == 3) launch_gl_stream_t<T, 3, 128>(iters);
+      else launch_gl_stream_t<T, 2, 128>(iters);
+    }
+  }
+  void launch_gl_stream(long long iters) {
+    if (f64()) launch_gl_stream_d<double>(iters);
+    else launch_gl_stream_d<float>(iters);
   }
 
   static size_t glpipe_smem(bool f64s, int d, int wb, int lmax) {
@@ -503,6 +550,12 @@ struct otdr_dev {
     touch(otdrk::gl_pipe_kernel<double, true, 4, 64>);
     touch(otdrk::gl_pipe_kernel<double, true, 6, 64>);
     touch(otdrk::gl_pipe_kernel<double, true, 8, 64>);
+    touch(otdrk::gl_stream_kernel<float, false, 2, 128>);
+    touch(otdrk::gl_stream_kernel<float, false, 3, 128>);
+    touch(otdrk::gl_stream_kernel<float, false, 4, 128>);
+    touch(otdrk::gl_stream_kernel<double, true, 2, 128>);
+    touch(otdrk::gl_stream_kernel<double, true, 3, 128>);
+    touch(otdrk::gl_stream_kernel<double, true, 4, 128>);
     touch(otdrk::gl_ring_kernel<float, false>);
     touch(otdrk::gl_ring_kernel<double, true>);
     touch(otdrk::gl_stage_kernel<float, false>);
@@ -737,7 +790,8 @@ struct otdr_dev {
     d_scnt = dalloc<unsigned>(size_t(S));
     CK(cudaMemset(d_scnt, 0, size_t(S) * sizeof(unsigned)));
     str_sspart = dalloc<double>(size_t(S));
-    str_part = dalloc<double>(size_t(P) * 4);
+    str_part = dalloc<double>(size_t(std::max<long long>(P, num_sms)) * 4);
+    str_part_cap = size_t(std::max<long long>(P, num_sms)) * 4;
     str_colpart = dalloc<double>(size_t(ntiles) * otdrk::kStreamTN);
     d_sfirst = dalloc<int>(first.size());
     CK(cudaMemcpy(d_sfirst, first.data(), first.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -940,6 +994,26 @@ struct otdr_dev {
           for (long long s0 = head; s0 < glp_nstr; s0 += 2)
             pos.push_back(int2{int(s0), int(std::min<long long>(2, glp_nstr - s0))});
           glp_groups = int(pos.size());
+          // persistent GL solve: one CTA per SM must be co-resident (cooperative)
+          gls_grid = 0;
+          {
+            int occ = 0;
+            const void* kern = f64() ? (glp_wb == 64 ? (const void*)otdrk::gl_stream_kernel<double, true, 4, 64>
+                                                     : (const void*)otdrk::gl_stream_kernel<double, true, 4, 128>)
+                                     : (glp_wb == 64 ? (const void*)otdrk::gl_stream_kernel<float, false, 4, 64>
+                                                     : (const void*)otdrk::gl_stream_kernel<float, false, 4, 128>);
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(glp_smem)));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, otdrk::kGLPThreads, glp_smem));
+            if (occ >= 1) {
+              gls_grid = num_sms;
+              if (const char* gg = std::getenv("OTDR_GL_PIPE_GRID")) gls_grid = std::max(1, std::min(gls_grid, std::atoi(gg)));
+              if (!str_part || str_part_cap < size_t(gls_grid) * 4) {
+                if (str_part) cudaFree(str_part);
+                str_part = dalloc<double>(size_t(std::max(gls_grid, 2 * num_sms)) * 4);
+                str_part_cap = size_t(std::max(gls_grid, 2 * num_sms)) * 4;
+              }
+            }
+          }
           if (d_glp_pos) cudaFree(d_glp_pos);
           d_glp_pos = dalloc<int2>(pos.size());
           CK(cudaMemcpy(d_glp_pos, pos.data(), pos.size() * sizeof(int2), cudaMemcpyHostToDevice));
@@ -1104,6 +1178,11 @@ struct otdr_dev {
       check_launch();
       return;
     }
+    if (iters > 0 && gl_stream_active(false, false)) {
+      launch_gl_stream(iters);
+      check_launch();
+      return;
+    }
     const int chunk = 16;
     if (iters >= chunk) {
       cudaGraphExec_t ex = get_graph(0, chunk, false, false);
@@ -1261,7 +1340,7 @@ const char* otdr_dev_last_error(const otdr_dev* ctx) { return ctx ? ctx->err.c_s
 int otdr_dev_solve_path(const otdr_dev* ctx) {
   if (!ctx) return OTDR_PATH_GRAPH;
   if (ctx->resident_active(false, false)) return OTDR_PATH_RESIDENT;
-  if (ctx->stream_active(false, false)) return OTDR_PATH_STREAM;
+  if (ctx->stream_active(false, false) || ctx->gl_stream_active(false, false)) return OTDR_PATH_STREAM;
   return OTDR_PATH_GRAPH;
 }
 
@@ -1390,6 +1469,7 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     if (const char* re = std::getenv("OTDR_RESIDENT")) ctx->allow_resident = std::strcmp(re, "off") != 0;
     if (const char* se = std::getenv("OTDR_SWEEP")) ctx->use_tma_sweep = std::strcmp(se, "tma") == 0;
     if (const char* st = std::getenv("OTDR_STREAM")) ctx->allow_stream = std::strcmp(st, "off") != 0;
+    if (const char* gs = std::getenv("OTDR_GL_STREAM")) ctx->allow_gl_stream = std::strcmp(gs, "off") != 0;
     ctx->str_d = -1;
     if (const char* tp = std::getenv("OTDR_STREAM_TILES")) ctx->str_tpc = std::max(1, std::atoi(tp));
     if (const char* tl = std::getenv("OTDR_STREAM_TAIL")) ctx->str_tail = std::max(1, std::atoi(tl));
@@ -1780,7 +1860,8 @@ otdr_status otdr_dev_time_steps(otdr_dev* ctx, double rho, int64_t iters, double
     ctx->prm.fused = 0;
     ctx->prm.record_trace = 0;
     ctx->push_prm();
-    if (iters >= 16 && !ctx->stream_active(false, false) && !ctx->resident_active(false, false))
+    if (iters >= 16 && !ctx->stream_active(false, false) && !ctx->resident_active(false, false) &&
+        !ctx->gl_stream_active(false, false))
       ctx->get_graph(0, 16, false, false);  // instantiate outside the timing
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -1900,7 +1981,8 @@ otdr_status otdr_dev_solve(otdr_dev* ctx, const otdr_solve_opts* o, otdr_solve_r
     // sweep compares each entry's old and new sign.
     CK(cudaStreamSynchronize(ctx->stream));
     const bool resident = ctx->resident_active(track, cert);
-    const bool streaming = !resident && ctx->stream_active(track, cert);
+    const bool gl_streaming = !resident && ctx->gl_stream_active(track, cert);
+    const bool streaming = !resident && (ctx->stream_active(track, cert) || gl_streaming);
     const bool use_while = ctx->comm == nullptr;
     const int body = 4;
     cudaGraphExec_t ex = nullptr;
@@ -1912,7 +1994,8 @@ otdr_status otdr_dev_solve(otdr_dev* ctx, const otdr_solve_opts* o, otdr_solve_r
       ctx->launch_resident(0);
       ctx->check_launch();
     } else if (streaming) {
-      ctx->launch_stream(0);
+      if (gl_streaming) ctx->launch_gl_stream(0);
+      else ctx->launch_stream(0);
       ctx->check_launch();
     } else if (use_while) {
       CK(cudaGraphLaunch(ex, ctx->stream));

@@ -64,16 +64,17 @@ __host__ __device__ inline size_t glpipe_smem_bytes(int Lmax) {
          size_t(kGLPMaxG) * W * 8 /* psi */ + 2 * size_t(kGLPWarps) * W * 8 /* red */ + 2 * W * 8 /* sig */;
 }
 
+// Sweeps work items claimed from *claim until none is left (all threads of the
+// CTA return together). Shared by the per-iteration gl_pipe_kernel and the
+// persistent gl_stream_kernel.
 template <typename T, bool EXACT, int D, int WB>
-__global__ void __launch_bounds__(kGLPThreads, 1) gl_pipe_kernel(GLPipeArgs A) {
+__device__ __forceinline__ void gl_pipe_items(const GLPipeArgs& A, unsigned* claim) {
   using V = typename Vec<T>::type;
   constexpr int VEC = Vec<T>::N;
   constexpr int W = WB / (int)sizeof(T);   // stripe width: WB (128 or 64) bytes per row
   constexpr int LPR = W / VEC;             // lanes per row (8 for 128-B stripes)
   constexpr int RPW = 32 / LPR;            // rows per warp instruction
   constexpr int RSTEP = kGLPWarps * RPW;   // rows per step
-  Ctl* ctl = A.ctl;
-  if (ctl->done) return;  // grid-uniform
   const Params& prm = *A.prm;
   const double rho = prm.rho, thr = prm.gl_thr;
   T* X = static_cast<T*>(A.X);
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(kGLPThreads, 1) gl_pipe_kernel(GLPipeArgs A) {
   const int nitems = A.nseg * A.ngroups;
 
   for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(&ctl->gl_ctr, 1u);
+    if (threadIdx.x == 0) s_item = atomicAdd(claim, 1u);
     __syncthreads();
     const int item = (int)s_item;
     if (item >= nitems) break;
@@ -258,6 +259,13 @@ __global__ void __launch_bounds__(kGLPThreads, 1) gl_pipe_kernel(GLPipeArgs A) {
       A.rowpart[(sg.begin + t) * (long long)A.ngroups + gi] = rowacc[t];
     __syncthreads();  // rowacc / phi_s / s_item reused by the next item
   }
+}
+
+template <typename T, bool EXACT, int D, int WB>
+__global__ void __launch_bounds__(kGLPThreads, 1) gl_pipe_kernel(GLPipeArgs A) {
+  Ctl* ctl = A.ctl;
+  if (ctl->done) return;  // grid-uniform
+  gl_pipe_items<T, EXACT, D, WB>(A, &ctl->gl_ctr);
   // the last CTA out resets the claim counter for the next launch
   if (threadIdx.x == 0) {
     __threadfence();
@@ -266,6 +274,245 @@ __global__ void __launch_bounds__(kGLPThreads, 1) gl_pipe_kernel(GLPipeArgs A) {
       ctl->gl_done = 0;
       __threadfence();
     }
+  }
+}
+
+}  // namespace otdrk
+
+namespace otdrk {
+
+// ---------------------------------------------------------------------------
+// Persistent group-lasso solve: the whole solve (or a step(k) run) in ONE
+// cooperative launch of one 512-thread CTA per SM, like stream_kernel
+// (otdr_stream.cuh) but with the pipelined GL sweep as phase A:
+//   A  gl_pipe_items: rowpart[row][position], colpart[segment][col]
+//   -- grid barrier --
+//   B  row folds (warp per row, position order) -> r, (sum r, sum r^2, sum R)
+//      column folds (thread per column, segment order) -> S_j; single GPU:
+//      s = S - q and sum s^2; row-sharded: S_j stored to every rank (NVLink)
+//   -- grid barrier --
+//   C  scalar folds in a fixed order (every CTA, identical), the peer exchange
+//      when sharded, the recurrence and the stopping logic (solver.cpp:179-235)
+struct GLStreamArgs {
+  GLPipeArgs g;
+  double* phi;
+  double* psi;
+  double* a;
+  double* b;
+  double* r;
+  double* s;
+  const double* p;
+  const double* q;
+  double* part;           // [P][4]
+  long long m_glob, n;
+  double* const* peers;   // nullptr: single GPU
+  double* rbuf;
+  unsigned long long* xep;
+  int rank, nranks;
+  long long iters;        // raw mode (prm.solving == 0)
+};
+
+template <typename T, bool EXACT, int D, int WB>
+__global__ void __launch_bounds__(kGLPThreads, 1) gl_stream_kernel(GLStreamArgs A) {
+  constexpr int NT = kGLPThreads, NW = kGLPWarps;
+  Ctl* ctl = A.g.ctl;
+  if (ctl->done) return;  // grid-uniform
+  const Params& prm = *A.g.prm;
+  __shared__ double sred[NW];
+  __shared__ double bc[4];
+  const int c = (int)blockIdx.x, P = (int)gridDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long m = A.g.m, n = A.n;
+  const long long gwarp = (long long)c * NW + warp, nwarps = (long long)P * NW;
+  const long long gtid = (long long)c * NT + threadIdx.x, nthr = (long long)P * NT;
+  const double dm = (double)A.m_glob, dn = (double)n, mn = (double)(A.m_glob + n);
+  const bool peer = A.peers != nullptr;
+  const int G = A.g.ngroups;
+  long long k = ctl->k;
+  double theta = ctl->theta[k & 1];
+  double best = ctl->best;
+  long long last_imp = ctl->last_improvement;
+  const long long k0 = ctl->k0;
+  long long it = 0;
+  const unsigned long long ebase = peer ? *A.xep : 0ull;
+  unsigned long long epoch = ebase + 1;
+
+  auto bsum = [&](double v) -> double {  // fixed-order block sum, valid in thread 0
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) sred[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+      for (int i = 0; i < NW; ++i) t += sred[i];
+    return t;
+  };
+
+  for (;;) {
+    // ---- A. pipelined group-lasso sweep
+    gl_pipe_items<T, EXACT, D, WB>(A.g, &ctl->gl_ctr);
+    grid_barrier(&ctl->bar_gls);
+
+    // ---- B. row folds and column folds
+    double sr = 0.0, sr2 = 0.0, sR = 0.0, ssq = 0.0;
+    for (long long i0 = gwarp * 4; i0 < m; i0 += nwarps * 4) {
+      double R[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int t = lane; t < G; t += 32) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i0 + u < m) R[u] += __ldcg(A.g.rowpart + (i0 + u) * G + t);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        R[u] = warp_sum(R[u]);
+        if (lane == 0 && i0 + u < m) {
+          const double ri = R[u] - A.p[i0 + u];
+          A.r[i0 + u] = ri;
+          sr += ri;
+          sr2 += ri * ri;
+          sR += R[u];
+        }
+      }
+    }
+    const int par = int(epoch & 1);
+    for (long long j = gtid; j < n; j += nthr) {
+      double S = 0.0;
+      for (int sg = 0; sg < A.g.nseg; ++sg) S += __ldcg(A.g.colpart + (long long)sg * A.g.ld + j);
+      if (peer) {
+        for (int rr = 0; rr < A.nranks; ++rr) xslot(A.peers[rr], par, A.rank, A.nranks, n)[j] = S;
+      } else {
+        const double sj = __dsub_rn(S, A.q[j]);
+        A.s[j] = sj;
+        ssq += sj * sj;
+      }
+    }
+    {
+      const double t1 = bsum(sr), t2 = bsum(sr2), t3 = bsum(sR), t4 = bsum(ssq);
+      if (threadIdx.x == 0) {
+        if (peer) __threadfence_system();  // this CTA's peer stores (cumulative through bar.sync)
+        A.part[c * 4 + 0] = t1;
+        A.part[c * 4 + 1] = t2;
+        A.part[c * 4 + 2] = t3;
+        A.part[c * 4 + 3] = t4;
+      }
+    }
+    grid_barrier(&ctl->bar_gls);
+
+    // ---- C. scalar folds, exchange, recurrence, stopping
+    if (c == 0 && threadIdx.x == 0) ctl->gl_ctr = 0;  // every CTA is past its last claim
+    if (peer) {
+      if (c == 0 && warp < 3) {
+        const double u = warp_fold_strided(A.part + warp, P, 4);
+        if (lane == 0)
+          for (int rr = 0; rr < A.nranks; ++rr) xslot(A.peers[rr], par, A.rank, A.nranks, n)[n + warp] = u;
+      }
+      if (c == 0) {
+        __syncthreads();
+        if (threadIdx.x == 0) xpublish(A.peers, A.rank, A.nranks, n, epoch);
+      }
+      if (threadIdx.x == 0) xwait(A.rbuf, A.nranks, n, epoch);
+      __syncthreads();
+      if (warp < 3 && lane == 0) {
+        double u = 0.0;
+        for (int rr = 0; rr < A.nranks; ++rr) u += __ldcg(xslot(A.rbuf, par, rr, A.nranks, n) + n + warp);
+        bc[warp] = u;
+      }
+      __syncthreads();
+      const double eta_p = __ddiv_rn(bc[0], mn);
+      const double shift_p = __dsub_rn(2.0 * eta_p, theta);
+      double ss = 0.0;
+      for (long long j = gtid; j < n; j += nthr) {
+        double S = 0.0;
+        for (int rr = 0; rr < A.nranks; ++rr) S += __ldcg(xslot(A.rbuf, par, rr, A.nranks, n) + j);
+        const double sj = __dsub_rn(S, A.q[j]), bj = A.b[j];
+        A.s[j] = sj;
+        ss += sj * sj;
+        A.psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift_p), dm);
+        A.b[j] = __dsub_rn(bj, sj);
+      }
+      for (long long i = gtid; i < m; i += nthr) {
+        const double ri = __ldcg(A.r + i), ai = A.a[i];
+        A.phi[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift_p), dn);
+        A.a[i] = __dsub_rn(ai, ri);
+      }
+      const double t4 = bsum(ss);
+      if (threadIdx.x == 0) A.part[c * 4 + 3] = t4;
+      grid_barrier(&ctl->bar_gls);  // phi / psi / s complete, ssq partials visible
+      if (warp == 0) {
+        const double u = warp_fold_strided(A.part + 3, P, 4);
+        if (lane == 0) bc[3] = u;
+      }
+      __syncthreads();
+    } else {
+      if (warp < 4) {
+        const double u = warp_fold_strided(A.part + warp, P, 4);
+        if (lane == 0) bc[warp] = u;
+      }
+      __syncthreads();
+      const double eta_l = __ddiv_rn(bc[0], mn);
+      const double shift_l = __dsub_rn(2.0 * eta_l, theta);
+      for (long long i = gtid; i < m; i += nthr) {
+        const double ri = __ldcg(A.r + i), ai = A.a[i];
+        A.phi[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift_l), dn);
+        A.a[i] = __dsub_rn(ai, ri);
+      }
+      for (long long j = gtid; j < n; j += nthr) {
+        const double sj = __ldcg(A.s + j), bj = A.b[j];
+        A.psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift_l), dm);
+        A.b[j] = __dsub_rn(bj, sj);
+      }
+    }
+    const double eta = __ddiv_rn(bc[0], mn);
+    const double nr2 = sqrt(bc[1]), ns2 = sqrt(bc[3]);
+    const double rp = (nr2 < ns2) ? ns2 : nr2;  // std::max semantics (solver.cpp:179)
+    theta = __dsub_rn(theta, eta);
+    ++k;
+    ++it;
+    ++epoch;
+    const long long kk = k - k0;
+    bool done = false;
+    int term = TERM_MAXITER;
+    if (prm.solving) {
+      if (!(rp - rp == 0.0)) {  // solver.cpp:181-185
+        done = true;
+        term = TERM_NONFINITE;
+      } else {
+        if (rp < best * (1.0 - 1e-14)) {  // solver.cpp:200-203
+          best = rp;
+          last_imp = kk;
+        }
+        const bool at_check = (kk % prm.check_every) == 0;
+        if (at_check && rp <= prm.tol_primal) {
+          done = true;
+          term = TERM_CONVERGED;
+        } else if (kk - last_imp >= 10000) {  // solver.cpp:17, :232-235
+          done = true;
+          term = TERM_STALLED;
+        } else if (kk >= prm.max_iter) {
+          done = true;
+          term = TERM_MAXITER;
+        }
+      }
+    } else if (it >= A.iters) {
+      done = true;
+    }
+    if (done) {
+      if (c == 0 && threadIdx.x == 0) {
+        ctl->k = k;
+        ctl->theta[k & 1] = theta;
+        ctl->eta = eta;
+        ctl->r_primal = rp;
+        ctl->best = best;
+        ctl->last_improvement = last_imp;
+        if (prm.solving) {
+          ctl->done = 1;
+          ctl->termination = term;
+        }
+        if (peer) *A.xep = epoch - 1;
+      }
+      break;
+    }
+    if (!peer) grid_barrier(&ctl->bar_gls);  // phi / psi complete before the next sweep
   }
 }
 

@@ -83,6 +83,7 @@ struct Ctl {
   unsigned int gl_ctr;         // pipelined group-lasso sweep: items claimed
   unsigned int gl_done;        //   CTAs finished (the last one resets both)
   unsigned int pad_;
+  unsigned long long bar_gls;  // persistent group-lasso solve kernel
 };
 
 struct TraceRow {

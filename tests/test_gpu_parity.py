@@ -727,13 +727,18 @@ def test_peer_exchange_ranks_on_one_gpu(ora, monkeypatch, storage, world, kind):
         e.close()
 
 
-def test_peer_exchange_group_lasso_graph_path(ora, monkeypatch):
+@pytest.mark.parametrize("mode", ["stream", "graph"])
+def test_peer_exchange_group_lasso(ora, monkeypatch, mode):
     """Group lasso on two rank contexts of one process, peers linked, no NCCL:
-    the graph loop's per-iteration exchange runs through p2p_allreduce_kernel.
+    the persistent GL solve kernel exchanges inside the kernel ("stream"), the
+    graph loop through p2p_allreduce_kernel ("graph", OTDR_GL_STREAM=off).
     Bands are cut at class boundaries; iterates match the unsharded oracle.
-    (The persistent GL grid is capped so a rank's spinning exchange kernel
-    never holds the SM the other rank's sweep still needs -- one GPU only.)"""
-    monkeypatch.setenv("OTDR_GL_PIPE_GRID", "100")
+    (The GL grid is capped so both ranks' persistent kernels are co-resident
+    and a spinning exchange kernel never holds an SM the other rank needs --
+    one GPU only.)"""
+    monkeypatch.setenv("OTDR_GL_PIPE_GRID", "70")
+    if mode == "graph":
+        monkeypatch.setenv("OTDR_GL_STREAM", "off")
     from paper_2305_18483_b200 import sharding
 
     m, n, classes = 1200, 500, 4
@@ -751,7 +756,7 @@ def test_peer_exchange_group_lasso_graph_path(ora, monkeypatch):
                           labels_local=np.asarray(ls)[lo:hi])
         engs.append(e)
     otdr.link_local(engs)
-    assert all(e.solve_path() == "graph" for e in engs)
+    assert all(e.solve_path() == mode for e in engs)
     _parallel([e.set_state for e in engs])
     rho = ora.default_stepsize(m, n)
     for _ in range(15):
@@ -878,3 +883,49 @@ def test_peer_exchange_device_cost_builder(ora, monkeypatch):
     assert rel(X, ref.X) <= 1e-12, rel(X, ref.X)
     for e in engs:
         e.close()
+
+
+@pytest.mark.parametrize("storage", ["f64", "f32"])
+@pytest.mark.parametrize("m,n,classes", [(1200, 900, 4), (3000, 700, 3), (1000, 1000, 10)])
+def test_gl_stream_kernel_matches_oracle_and_graph(ora, monkeypatch, storage, m, n, classes):
+    """Persistent group-lasso solve (gl_stream_kernel, one launch) against the
+    oracle after k steps, and a full solve against the graph loop
+    (OTDR_GL_STREAM=off): same termination and iteration count."""
+    C, p, q, src, tgt, ls, lt = ora.adaptation_problem(m, n, classes, 13)
+    Co = C if storage == "f64" else C.astype(np.float32).astype(np.float64)
+    pr = ora.Problem(Co, p, q)
+    offs, cells = ora.column_class_blocks(ls, n)
+    oreg = ora.group_lasso_reg(2e-3, offs, cells)
+    st = ora.make_state(pr)
+    reg = otdr.GroupLassoReg(2e-3, otdr.column_class_blocks(ls, n))
+    eng = otdr.Engine(m, n, storage)
+    eng.set_problem(C, p, q)
+    eng.set_regularizer(reg)
+    eng.set_state()
+    assert eng.solve_path() == "stream"
+    rho = ora.default_stepsize(m, n)
+    tol = 1e-12 if storage == "f64" else 1e-5
+    done = 0
+    for k in (1, 8, 30):
+        for _ in range(k - done):
+            ora.step(st, pr, oreg, rho)
+        eng.step(rho, k - done)
+        done = k
+        g = eng.get_state()
+        assert g.k == k
+        assert rel(g.X, st.X) <= tol, (k, rel(g.X, st.X))
+        assert rel(g.phi, st.phi) <= tol and rel(g.psi, st.psi) <= tol
+    eng.set_state()
+    a = eng.solve(otdr.SolverOptions(tol_primal=1e-5, max_iter=5000, storage=storage), with_state=False)
+    eng.close()
+    monkeypatch.setenv("OTDR_GL_STREAM", "off")
+    eng = otdr.Engine(m, n, storage)
+    eng.set_problem(C, p, q)
+    eng.set_regularizer(reg)
+    eng.set_state()
+    assert eng.solve_path() == "graph"
+    b = eng.solve(otdr.SolverOptions(tol_primal=1e-5, max_iter=5000, storage=storage), with_state=False)
+    eng.close()
+    assert a.termination == b.termination
+    assert abs(a.iterations - b.iterations) <= (0 if storage == "f64" else 2)
+    assert abs(a.objective - b.objective) <= (1e-9 if storage == "f64" else 1e-6) * abs(b.objective)
