@@ -929,3 +929,23 @@ def test_gl_stream_kernel_matches_oracle_and_graph(ora, monkeypatch, storage, m,
     assert a.termination == b.termination
     assert abs(a.iterations - b.iterations) <= (0 if storage == "f64" else 2)
     assert abs(a.objective - b.objective) <= (1e-9 if storage == "f64" else 1e-6) * abs(b.objective)
+
+
+@pytest.mark.parametrize("path", ["resident", "stream", "gl_stream", "graph"])
+def test_nonfinite_every_device_loop(ora, monkeypatch, path):
+    """solver.cpp:181-185 through every device loop: a warm start that
+    overflows on the first step raises NonFiniteIterate with the reference's
+    message at iteration 1 (the persistent kernels stop inside the launch)."""
+    if path != "resident":
+        monkeypatch.setenv("OTDR_RESIDENT", "off")
+    if path == "graph":
+        monkeypatch.setenv("OTDR_STREAM", "off")
+        monkeypatch.setenv("OTDR_GL_STREAM", "off")
+    m, n = 300, 280
+    C, p, q, *_ = ora.gaussian_problem(m, n, 3)
+    pr = otdr.validate_problem(C, p, q)
+    reg = (otdr.GroupLassoReg(1e-3, otdr.column_class_blocks([i % 3 for i in range(m)], n))
+           if path == "gl_stream" else otdr.ZeroReg())
+    init = otdr.WarmStart(np.full((m, n), 1e308), np.zeros(m), np.zeros(n))
+    with pytest.raises(otdr.NonFiniteIterate, match="non-finite iterate at iteration 1"):
+        otdr.solve(pr, reg, otdr.SolverOptions(init=init, storage="f64"))
