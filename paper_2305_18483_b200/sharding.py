@@ -74,22 +74,38 @@ def broadcast_nccl_id(dist, rank: int) -> bytes:
     return obj[0]
 
 
-def connect_peers(dist, eng: Engine) -> bool:
+def connect_peers(dist, eng: Engine, device: Optional[int] = None) -> bool:
     """All-gather every rank's receive-buffer IPC handle and import them, so
     the solve loop exchanges column sums over NVLink peer memory inside the
-    streaming kernel (collective). Returns False -- keeping the NCCL
-    exchange -- when a peer's buffer cannot be mapped (no P2P path)."""
-    handles = [None] * dist.get_world_size()
-    dist.all_gather_object(handles, eng.peer_export())
+    streaming kernel (collective). Returns False -- the context keeps its NCCL
+    exchange -- when some pair of the ranks' GPUs has no peer access; raises
+    if a handle that should map does not."""
+    world = dist.get_world_size()
+    ok = 1
     try:
-        eng.peer_import(handles)
+        import torch
+
+        dev = torch.cuda.current_device() if device is None else device
+        devs = [None] * world
+        dist.all_gather_object(devs, dev)
+        ok = int(all(d == dev or torch.cuda.can_device_access_peer(dev, d) for d in devs))
+    except Exception:  # no torch / no CUDA runtime view: let the import decide
         ok = 1
-    except Exception:
-        ok = 0
-    flags = [None] * dist.get_world_size()
+    flags = [None] * world
     dist.all_gather_object(flags, ok)
     if not all(flags):
-        raise RuntimeError("peer-memory exchange could not be set up on every rank")
+        return False
+    handles = [None] * world
+    dist.all_gather_object(handles, eng.peer_export())
+    err = ""
+    try:
+        eng.peer_import(handles)
+    except Exception as e:  # pragma: no cover - hardware dependent
+        err = str(e) or type(e).__name__
+    errs = [None] * world
+    dist.all_gather_object(errs, err)
+    if any(errs):
+        raise RuntimeError("peer-memory exchange could not be set up: " + "; ".join(e for e in errs if e))
     return True
 
 
