@@ -980,7 +980,7 @@ struct otdr_dev {
         if (glp_smem) {
           const long long W = glp_wb / (long long)esz;
           glp_nstr = int((ld + W - 1) / W);
-          glp_G = 8;
+          glp_G = 10;
           if (const char* ge = std::getenv("OTDR_GL_PIPE_G"))
             glp_G = std::max(1, std::min(otdrk::kGLPMaxG, std::atoi(ge)));
           // stripe positions: runs of glp_G stripes, then runs of 2 for the
