@@ -9,7 +9,7 @@
 // 125 KB for a 1000-row class in fp32).
 //
 // One persistent CTA per SM (512 threads) claims work items -- (segment,
-// position = run of up to 8 consecutive stripes) -- from an atomic counter,
+// position = run of up to 10 consecutive stripes) -- from an atomic counter,
 // position-major, so the short positions at the end of the stripe range
 // (2 stripes) are the last claims and CTA finish times stay close. Inside an item
 // the stripes are pipelined row by row through the SAME staging buffer:
