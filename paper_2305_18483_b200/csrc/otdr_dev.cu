@@ -842,7 +842,7 @@ struct otdr_dev {
   }
 
   bool stream_active(bool track, bool cert) const {
-    return str_P > 0 && res_G == 0 && !track && !cert && !prm.fused;
+    return str_P > 0 && res_G == 0 && !track && !cert && (!prm.fused || str_d > 0);
   }
 
   void launch_stream(long long iters) {

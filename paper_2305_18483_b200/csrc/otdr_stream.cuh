@@ -273,7 +273,8 @@ template <typename T, int REG, bool EXACT, int NV, int D>
 __device__ __forceinline__ void stream_segment_async(const StreamArgs& A, int tile, long long stripe,
                                                      long long r0, long long r1, double rho,
                                                      double qd, double qinv,
-                                                     double (*red)[kStreamTN], uint4* q) {
+                                                     double (*red)[kStreamTN], uint4* q,
+                                                     int mode = MODE_NORMAL) {
   using V = typename Vec<T>::type;
   constexpr int VEC = Vec<T>::N;
   constexpr int NS = 2 * NV + 1;  // 16-byte slots per row: X[NV], C[NV], phi
@@ -305,7 +306,7 @@ __device__ __forceinline__ void stream_segment_async(const StreamArgs& A, int ti
       for (int v = 0; v < NV; ++v)
         if (cok[v]) {
           cp_async16(slot(st, v), xrow + cols[v], pfirst);
-          cp_async16(slot(st, NV + v), crow + cols[v], pfirst);
+          if (mode != MODE_ODD) cp_async16(slot(st, NV + v), crow + cols[v], pfirst);  // odd: B only
         }
       cp_async16(slot(st, 2 * NV), A.phi + (i & ~1LL));
     }
@@ -327,15 +328,19 @@ __device__ __forceinline__ void stream_segment_async(const StreamArgs& A, int ti
       if (!cok[v]) continue;
       double x[VEC], cc[VEC], o[VEC];
       unpack(*reinterpret_cast<const V*>(slot(st, v)), x);
-      unpack(*reinterpret_cast<const V*>(slot(st, NV + v)), cc);
+      if (mode != MODE_ODD) unpack(*reinterpret_cast<const V*>(slot(st, NV + v)), cc);
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
-        const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, cc[e])), ph),
-                                             psi_r[v][e])
-                                 : (fma(-rho, cc[e], x[e]) + ph) + psi_r[v][e];
+        double val;
+        if (mode == MODE_ODD)  // B + phi + psi (solver.cpp:170-172): the buffer holds B = X - rho C
+          val = EXACT ? __dadd_rn(__dadd_rn(x[e], ph), psi_r[v][e]) : (x[e] + ph) + psi_r[v][e];
+        else
+          val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, cc[e])), ph), psi_r[v][e])
+                      : (fma(-rho, cc[e], x[e]) + ph) + psi_r[v][e];
         double nx = clamp0(val);
         if (REG == REG_QUAD) nx = EXACT ? div_rn_by(nx, qd, qinv) : nx * qinv;
-        o[e] = nx;
+        // even step of the fused path stores B = (-rho C) + X_{k+1} (solver.cpp:162,167)
+        o[e] = mode == MODE_EVEN ? (EXACT ? __dadd_rn(-__dmul_rn(rho, cc[e]), nx) : nx - rho * cc[e]) : nx;
         cacc[v][e] += nx;
         rs += nx;
       }
@@ -439,6 +444,9 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
   const bool peer = A.peers != nullptr;
   const unsigned long long ebase = peer ? *A.xep : 0ull;
   unsigned long long epoch = ebase + 1;
+  // fused even/odd path (solver.cpp:127-177): the X buffer alternates
+  // between X (even iterations read C) and B = X - rho C (odd ones do not)
+  int shifted = prm.fused ? ctl->fused_shifted : 0;
 
   auto stamp = [&](int slot) {
     if (A.tstamp && it < kTraceIters && threadIdx.x == 0 && (slot < P ? true : c == 0))
@@ -446,6 +454,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
   };
   for (;;) {
     stamp(P + 0);
+    const int fmode = prm.fused ? (shifted ? MODE_ODD : MODE_EVEN) : MODE_NORMAL;
     // ---- A. sweep tiles claimed from the iteration's tile counter
     for (;;) {
       if (threadIdx.x == 0) s_tile = atomicAdd(&ctl->tile_ctr, 1u);
@@ -473,7 +482,8 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
         tl.z = (int)((r0_ + R_ < m) ? r0_ + R_ : m);
       }
       if constexpr (D > 0) {
-        stream_segment_async<T, REG, EXACT, NV, D>(A, tile, tl.x, tl.y, tl.z, rho, qd, qinv, red, squeue);
+        stream_segment_async<T, REG, EXACT, NV, D>(A, tile, tl.x, tl.y, tl.z, rho, qd, qinv, red, squeue,
+                                                   fmode);
       } else {
         stream_segment<T, REG, EXACT, NV, U>(A, tile, tl.x, tl.y, tl.z, rho, qd, qinv, red);
       }
@@ -605,6 +615,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
     ++k;
     ++it;
     ++epoch;
+    if (prm.fused) shifted ^= 1;
     const long long kk = k - k0;
     bool done = false;
     int term = TERM_MAXITER;
@@ -644,6 +655,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
           ctl->done = 1;
           ctl->termination = term;
         }
+        ctl->fused_shifted = shifted;
         if (peer) *A.xep = epoch - 1;  // every CTA read the base at entry
       }
       break;

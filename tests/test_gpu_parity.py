@@ -949,3 +949,29 @@ def test_nonfinite_every_device_loop(ora, monkeypatch, path):
     init = otdr.WarmStart(np.full((m, n), 1e308), np.zeros(m), np.zeros(n))
     with pytest.raises(otdr.NonFiniteIterate, match="non-finite iterate at iteration 1"):
         otdr.solve(pr, reg, otdr.SolverOptions(init=init, storage="f64"))
+
+
+@pytest.mark.parametrize("max_iter", [40, 41])  # ends after an odd / an even (shifted) iteration
+@pytest.mark.parametrize("kind,param", [("none", 0.0), ("quad", 0.9)])
+def test_fused_stream_kernel_matches_oracle(ora, monkeypatch, kind, param, max_iter):
+    """SolverOptions.fused (solver.cpp:127-177) on the streaming kernel, fp64:
+    even iterations store B = X - rho C, odd ones read B and never C. Same
+    iterations, plan (un-shifted when the run ends on an even step), phi and
+    objective as the oracle's fused solve."""
+    monkeypatch.setenv("OTDR_RESIDENT", "off")
+    m, n = 700, 600
+    C, p, q, *_ = ora.gaussian_problem(m, n, 23)
+    pr = ora.Problem(C, p, q)
+    o = ora.solve(pr, oracle_reg(ora, kind, param, None, n), max_iter=max_iter, tol_primal=1e-300,
+                  fused=True)
+    eng = otdr.Engine(m, n, "f64")
+    eng.set_problem(C, p, q)
+    eng.set_regularizer(dev_reg(kind, param, None, n))
+    eng.set_state()
+    assert eng.solve_path() == "stream"
+    rep = eng.solve(otdr.SolverOptions(max_iter=max_iter, tol_primal=1e-300, fused=True, storage="f64"))
+    eng.close()
+    assert rep.iterations == o.iterations == max_iter
+    assert rel(rep.plan(), o.state.X) <= 1e-12, rel(rep.plan(), o.state.X)
+    assert rel(rep.state.phi, o.state.phi) <= 1e-12 and rel(rep.state.psi, o.state.psi) <= 1e-12
+    assert abs(rep.objective - o.objective) <= 1e-11 * abs(o.objective)
