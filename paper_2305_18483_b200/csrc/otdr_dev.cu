@@ -1981,8 +1981,12 @@ otdr_status otdr_dev_solve(otdr_dev* ctx, const otdr_solve_opts* o, otdr_solve_r
     // sweep compares each entry's old and new sign.
     CK(cudaStreamSynchronize(ctx->stream));
     const bool resident = ctx->resident_active(track, cert);
-    const bool gl_streaming = !resident && ctx->gl_stream_active(track, cert);
-    const bool streaming = !resident && (ctx->stream_active(track, cert) || gl_streaming);
+    // tol_gap without a trace runs on the persistent kernels: a launch stops at
+    // a check iteration with r_primal <= tol and the certificate kernels decide
+    const bool gap_only = o->has_tol_gap && !track && !o->fused;
+    const bool pcert = cert && !gap_only;
+    const bool gl_streaming = !resident && ctx->gl_stream_active(track, pcert);
+    const bool streaming = !resident && (ctx->stream_active(track, pcert) || gl_streaming);
     const bool use_while = ctx->comm == nullptr;
     const int body = 4;
     cudaGraphExec_t ex = nullptr;
@@ -1994,9 +1998,18 @@ otdr_status otdr_dev_solve(otdr_dev* ctx, const otdr_solve_opts* o, otdr_solve_r
       ctx->launch_resident(0);
       ctx->check_launch();
     } else if (streaming) {
-      if (gl_streaming) ctx->launch_gl_stream(0);
-      else ctx->launch_stream(0);
-      ctx->check_launch();
+      for (;;) {
+        if (gl_streaming) ctx->launch_gl_stream(0);
+        else ctx->launch_stream(0);
+        ctx->check_launch();
+        if (!gap_only) break;
+        ctx->pull_ctl();
+        if (ctx->h_ctl->done || !ctx->h_ctl->want_cert) break;
+        ctx->launch_cert(0, 0, 0);  // certificate + the reference's stopping decision
+        ctx->check_launch();
+        ctx->pull_ctl();
+        if (ctx->h_ctl->done) break;
+      }
     } else if (use_while) {
       CK(cudaGraphLaunch(ex, ctx->stream));
     } else {

@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
     ++epoch;
     if (prm.fused) shifted ^= 1;
     const long long kk = k - k0;
-    bool done = false;
+    bool done = false, want_cert = false;
     int term = TERM_MAXITER;
     if (prm.solving) {
       if (!(rp - rp == 0.0)) {  // solver.cpp:181-185
@@ -629,7 +629,11 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
           last_imp = kk;
         }
         const bool at_check = (kk % prm.check_every) == 0;
-        if (at_check && rp <= prm.tol_primal) {
+        if (at_check && rp <= prm.tol_primal && prm.has_tol_gap) {
+          // tol_gap: the launch ends here; the host runs the certificate
+          // kernels, whose finisher applies converged / stalled / max_iter
+          want_cert = true;
+        } else if (at_check && rp <= prm.tol_primal) {
           done = true;
           term = TERM_CONVERGED;
         } else if (kk - last_imp >= 10000) {  // solver.cpp:17, :232-235
@@ -643,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
     } else if (it >= A.iters) {
       done = true;
     }
-    if (done) {
+    if (done || want_cert) {
       if (c == 0 && threadIdx.x == 0) {
         ctl->k = k;
         ctl->theta[k & 1] = theta;
@@ -651,7 +655,8 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
         ctl->r_primal = rp;
         ctl->best = best;
         ctl->last_improvement = last_imp;
-        if (prm.solving) {
+        ctl->want_cert = want_cert ? 1 : 0;
+        if (prm.solving && done) {
           ctl->done = 1;
           ctl->termination = term;
         }

@@ -975,3 +975,29 @@ def test_fused_stream_kernel_matches_oracle(ora, monkeypatch, kind, param, max_i
     assert rel(rep.plan(), o.state.X) <= 1e-12, rel(rep.plan(), o.state.X)
     assert rel(rep.state.phi, o.state.phi) <= 1e-12 and rel(rep.state.psi, o.state.psi) <= 1e-12
     assert abs(rep.objective - o.objective) <= 1e-11 * abs(o.objective)
+
+
+@pytest.mark.parametrize("kind,param,tol_gap", [("quad", 0.5, 1e-7), ("none", 0.0, 1e-6), ("gl", 1e-3, 1e-6)])
+def test_tol_gap_on_persistent_kernels(ora, monkeypatch, kind, param, tol_gap):
+    """tol_gap (solver.cpp:205-219) on the persistent kernels: a launch stops at
+    every check iteration with r_primal <= tol, the certificate kernels decide
+    (Converged / continue / Stalled / MaxIter), the host relaunches. Same
+    termination, iteration count and final objective as the oracle."""
+    monkeypatch.setenv("OTDR_RESIDENT", "off")
+    m, n = 400, 350
+    C, p, q, *_ = ora.gaussian_problem(m, n, 29)
+    labels = [i % 4 for i in range(m)]
+    pr = ora.Problem(C, p, q)
+    o = ora.solve(pr, oracle_reg(ora, kind, param, labels, n), tol_primal=1e-6, tol_gap=tol_gap,
+                  check_every=5, max_iter=30000)
+    eng = otdr.Engine(m, n, "f64")
+    eng.set_problem(C, p, q)
+    eng.set_regularizer(dev_reg(kind, param, labels, n))
+    eng.set_state()
+    assert eng.solve_path() == "stream"
+    rep = eng.solve(otdr.SolverOptions(tol_primal=1e-6, tol_gap=tol_gap, check_every=5, max_iter=30000,
+                                       storage="f64"))
+    eng.close()
+    assert rep.termination.name == o.termination
+    assert rep.iterations == o.iterations
+    assert abs(rep.objective - o.objective) <= 1e-10 * abs(o.objective)
