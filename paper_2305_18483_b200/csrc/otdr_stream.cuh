@@ -269,12 +269,11 @@ __host__ __device__ constexpr size_t stream_async_smem() {
   return size_t(D) * size_t(2 * NV + 1) * kThreads * 16;
 }
 
-template <typename T, int REG, bool EXACT, int NV, int D>
+template <typename T, int REG, bool EXACT, int NV, int D, int mode = MODE_NORMAL>
 __device__ __forceinline__ void stream_segment_async(const StreamArgs& A, int tile, long long stripe,
                                                      long long r0, long long r1, double rho,
                                                      double qd, double qinv,
-                                                     double (*red)[kStreamTN], uint4* q,
-                                                     int mode = MODE_NORMAL) {
+                                                     double (*red)[kStreamTN], uint4* q) {
   using V = typename Vec<T>::type;
   constexpr int VEC = Vec<T>::N;
   constexpr int NS = 2 * NV + 1;  // 16-byte slots per row: X[NV], C[NV], phi
@@ -482,8 +481,12 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
         tl.z = (int)((r0_ + R_ < m) ? r0_ + R_ : m);
       }
       if constexpr (D > 0) {
-        stream_segment_async<T, REG, EXACT, NV, D>(A, tile, tl.x, tl.y, tl.z, rho, qd, qinv, red, squeue,
-                                                   fmode);
+        if (fmode == MODE_EVEN)
+          stream_segment_async<T, REG, EXACT, NV, D, MODE_EVEN>(A, tile, tl.x, tl.y, tl.z, rho, qd, qinv, red, squeue);
+        else if (fmode == MODE_ODD)
+          stream_segment_async<T, REG, EXACT, NV, D, MODE_ODD>(A, tile, tl.x, tl.y, tl.z, rho, qd, qinv, red, squeue);
+        else
+          stream_segment_async<T, REG, EXACT, NV, D>(A, tile, tl.x, tl.y, tl.z, rho, qd, qinv, red, squeue);
       } else {
         stream_segment<T, REG, EXACT, NV, U>(A, tile, tl.x, tl.y, tl.z, rho, qd, qinv, red);
       }
