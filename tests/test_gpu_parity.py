@@ -669,6 +669,7 @@ def _parallel(fns):
     return out
 
 
+@pytest.mark.timeout(240, method="thread")  # a hung exchange must not hang the suite
 @pytest.mark.parametrize("storage", ["f64", "f32"])
 @pytest.mark.parametrize("world,kind", [(2, "quad"), (3, "none")])
 def test_peer_exchange_ranks_on_one_gpu(ora, monkeypatch, storage, world, kind):
@@ -727,6 +728,7 @@ def test_peer_exchange_ranks_on_one_gpu(ora, monkeypatch, storage, world, kind):
         e.close()
 
 
+@pytest.mark.timeout(240, method="thread")  # a hung exchange must not hang the suite
 @pytest.mark.parametrize("mode", ["stream", "graph"])
 def test_peer_exchange_group_lasso(ora, monkeypatch, mode):
     """Group lasso on two rank contexts of one process, peers linked, no NCCL:
@@ -852,6 +854,7 @@ def test_first_step_bitwise(ora, monkeypatch, kind, param, resident):
         assert np.array_equal(g.X, st.X), int((g.X != st.X).sum())
 
 
+@pytest.mark.timeout(240, method="thread")  # a hung exchange must not hang the suite
 def test_peer_exchange_device_cost_builder(ora, monkeypatch):
     """Row-sharded device cost builder without NCCL: the normalising maximum
     of squared_distance_cost (problem.cpp:68-74) is all-reduced (max) over

@@ -20,6 +20,7 @@ def _free_port():
     return port
 
 
+@pytest.mark.timeout(300, method="thread")
 def test_peer_ipc_two_processes():
     env = dict(os.environ, OTDR_STREAM_GRID="64")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
