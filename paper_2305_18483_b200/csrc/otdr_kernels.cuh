@@ -1458,15 +1458,18 @@ struct FinalizeArgs {
 __device__ __forceinline__ void grid_barrier(unsigned long long* counter) {
   // Arrival number a belongs to generation a / gridDim.x; wait until the
   // counter reaches the end of that generation (one atomic + one polled word).
+  // The arrival is a gpu-scope release (cumulative over the CTA's writes that
+  // bar.sync ordered before it), the poll a gpu-scope acquire: no separate
+  // full fences on either side.
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned long long arrived = atomicAdd(counter, 1ull);
+    unsigned long long arrived;
+    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(arrived) : "l"(counter) : "memory");
     const unsigned long long target = (arrived / gridDim.x + 1ull) * gridDim.x;
-    volatile unsigned long long* cnt = counter;
-    while (*cnt < target) {
-    }
-    __threadfence();
+    unsigned long long cur;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(counter) : "memory");
+    } while (cur < target);
   }
   __syncthreads();
 }
