@@ -264,7 +264,7 @@ struct otdr_dev {
     otdrk::GLPipeArgs ga{X, C, phi, psi, rowpart, colpart, d_seg, d_glp_pos, d_prm, d_ctl, m_loc, ld,
                          num_segs, glp_nstr, glp_groups, glp_lmax};
     // OTDR_GL_PIPE_GRID caps the persistent grid (several ranks sharing one GPU in tests)
-    static const int cap = std::getenv("OTDR_GL_PIPE_GRID") ? std::atoi(std::getenv("OTDR_GL_PIPE_GRID")) : 0;
+    const int cap = std::getenv("OTDR_GL_PIPE_GRID") ? std::atoi(std::getenv("OTDR_GL_PIPE_GRID")) : 0;
     const int grid = cap > 0 ? std::min(cap, num_sms) : num_sms;
     kern<<<grid, otdrk::kGLPThreads, glp_smem, stream>>>(ga);
   }
@@ -764,7 +764,7 @@ struct otdr_dev {
     // about str_tpc long tiles per CTA (OTDR_STREAM_TILES)
     // (>= 128 rows: shorter tiles cost more in pipeline fill and partial
     // folds than they gain in balance -- measured at 4000^2)
-    static const long long min_rows = std::getenv("OTDR_STREAM_MINROWS") ? std::atoll(std::getenv("OTDR_STREAM_MINROWS")) : 128;
+    const long long min_rows = std::getenv("OTDR_STREAM_MINROWS") ? std::atoll(std::getenv("OTDR_STREAM_MINROWS")) : 128;
     const long long big = std::min<long long>(
         std::max<long long>(1, m_loc), std::max<long long>(min_rows, (m_loc * S + str_tpc * P - 1) / (str_tpc * P)));
     // short tail tiles: a quarter of a long tile, but >= 96 rows (smaller tiles
