@@ -43,7 +43,8 @@ struct otdr_batch {
   int bs_nch = 0, bs_nsets = 0;
   size_t bs_smem = 0;
   static constexpr int kBSD = 6;
-  int bs_nt = 512;  // threads per problem CTA (OTDR_BATCH_THREADS=256: two CTAs per SM)
+  int bs_nt = 256;  // threads per problem CTA (OTDR_BATCH_THREADS=512: one CTA per SM)
+  int bs_cs = 2;    // CTAs per problem (OTDR_BATCH_CLUSTER=1: one CTA per problem)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::string err;
@@ -78,19 +79,36 @@ struct otdr_batch {
     BCK(cudaMemcpy(C, buf.data(), buf.size() * sizeof(T), cudaMemcpyHostToDevice));
   }
 
-  template <typename T, int NT>
+  template <typename T, int NT, int CS>
   void launch_stream_nt() {
-    auto kern = otdrk::bstream_kernel<T, sizeof(T) == 8, kBSD, NT>;
+    auto kern = otdrk::bstream_kernel<T, sizeof(T) == 8, kBSD, NT, CS>;
     BCK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bs_smem)));
     otdrk::BStreamArgs ba{X, C, m * ld, phi, a, r, p, psi, b, s, q, ctl, prm, m, n, ld,
                           bs_nch, bs_nsets, reg == OTDR_REG_QUAD ? otdrk::REG_QUAD : otdrk::REG_NONE};
-    kern<<<unsigned(B), NT, bs_smem, stream>>>(ba);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(unsigned(B * CS), 1, 1);
+    lc.blockDim = dim3(NT, 1, 1);
+    lc.dynamicSmemBytes = bs_smem;
+    lc.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(CS);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    BCK(cudaLaunchKernelEx(&lc, kern, ba));
     BCK(cudaGetLastError());
   }
   template <typename T>
   void launch_stream() {
-    if (bs_nt == 512) launch_stream_nt<T, 512>();
-    else launch_stream_nt<T, 256>();
+    if (bs_cs == 2) {
+      if (bs_nt == 512) launch_stream_nt<T, 512, 2>();
+      else launch_stream_nt<T, 256, 2>();
+    } else {
+      if (bs_nt == 512) launch_stream_nt<T, 512, 1>();
+      else launch_stream_nt<T, 256, 1>();
+    }
   }
 
   template <typename T>
@@ -178,7 +196,8 @@ otdr_status otdr_batch_create(int device, otdr_storage storage, int64_t batch, i
     {  // streaming mode (default when it fits): one CTA per problem
       const long long vecw = 32 * (bt->f64() ? 2 : 4);
       const long long nch = (bt->ld + vecw - 1) / vecw;
-      if (const char* bn = std::getenv("OTDR_BATCH_THREADS")) bt->bs_nt = std::atoi(bn) == 256 ? 256 : 512;
+      if (const char* bn = std::getenv("OTDR_BATCH_THREADS")) bt->bs_nt = std::atoi(bn) == 512 ? 512 : 256;
+      if (const char* bc = std::getenv("OTDR_BATCH_CLUSTER")) bt->bs_cs = std::atoi(bc) == 1 ? 1 : 2;
       const int nw = bt->bs_nt / 32;
       if (nch <= nw) {
         bt->bs_nch = int(nch);

@@ -42,19 +42,26 @@ struct BStreamArgs {
 
 template <typename T, int D, int NT>
 __host__ __device__ inline size_t bstream_smem_bytes(long long m, long long ld, int nch, int nsets) {
-  return size_t(D) * 2 * NT * 16 + size_t(4 * m + 4 * ld + m * nch + (long long)nsets * ld) * 8 +
-         size_t(NT / 32 + 8) * 8;
+  return size_t(D) * 2 * NT * 16 + size_t(4 * m + 5 * ld + m * nch + (long long)nsets * ld) * 8 +
+         size_t(NT / 32 + 16) * 8;
 }
 
-template <typename T, bool EXACT, int D, int NT>
+// CS > 1: a thread-block cluster of CS CTAs per problem, each streaming a
+// band of the rows; the column partials and the three row scalars are
+// combined over distributed shared memory in cluster-rank order (identical in
+// every CTA), so the problem runs CS times faster -- the batch's tail is its
+// slowest problems, which otherwise run on one SM each.
+template <typename T, bool EXACT, int D, int NT, int CS>
 __global__ void __launch_bounds__(NT, 512 / NT) bstream_kernel(BStreamArgs A) {
+  namespace cg = cooperative_groups;
   constexpr int kBST = NT;
   constexpr int kBSW = NT / 32;
   using V = typename Vec<T>::type;
   constexpr int VEC = Vec<T>::N;
-  const int prob = blockIdx.x;
+  const int prob = blockIdx.x / CS;
+  const int crank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
   Ctl* ctl = A.ctl + prob;
-  if (ctl->done) return;
+  if (ctl->done) return;  // uniform over the cluster
   const Params& prm = *A.prm;
   const long long m = A.m, n = A.n, ld = A.ld;
   const int nch = A.nch, nsets = A.nsets;
@@ -73,11 +80,15 @@ __global__ void __launch_bounds__(NT, 512 / NT) bstream_kernel(BStreamArgs A) {
   double* q_s = s_s + ld;
   double* rowp = q_s + ld;                 // [m][nch]
   double* colbuf = rowp + m * nch;         // [nsets][ld]
-  double* red = colbuf + (long long)nsets * ld;  // [kBSW]
+  double* cpart = colbuf + (long long)nsets * ld;  // [ld] this CTA's column sums
+  double* red = cpart + ld;                // [kBSW]
   double* bc = red + kBSW;                 // [8]
+  double* xs = bc + 8;                     // [8] this CTA's row scalars (DSMEM-visible)
+  // rows of this CTA's band
+  const long long rb = m * crank / CS, re = m * (crank + 1) / CS;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (long long i = threadIdx.x; i < m; i += kBST) {
+  for (long long i = rb + threadIdx.x; i < re; i += kBST) {
     phi_s[i] = A.phi[prob * m + i];
     a_s[i] = A.a[prob * m + i];
     r_s[i] = A.r[prob * m + i];
@@ -117,9 +128,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) bstream_kernel(BStreamArgs A) {
         ps[e] = cok ? psi_s[cb + e] : 0.0;
         cacc[e] = 0.0;
       }
-      long long iss = set;
+      long long iss = rb + set;
       auto issue = [&](int st) {
-        if (iss < m && cok) {
+        if (iss < re && cok) {
           cp_async16(slot(st, 0), Xg + iss * ld + cb);
           cp_async16(slot(st, 1), Cg + iss * ld + cb);
         }
@@ -129,7 +140,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) bstream_kernel(BStreamArgs A) {
 #pragma unroll
       for (int d = 0; d < D - 1; ++d) issue(d);
       int st = 0;
-      for (long long i = set; i < m; i += nsets) {
+      for (long long i = rb + set; i < re; i += nsets) {
         issue(st == 0 ? D - 1 : st - 1);
         cp_async_wait<D - 1>();
         double rs = 0.0;
@@ -161,39 +172,62 @@ __global__ void __launch_bounds__(NT, 512 / NT) bstream_kernel(BStreamArgs A) {
       }
     }
     __syncthreads();
-    // ---- folds: rows (chunk order), columns (row-set order)
-    double sr = 0.0, sr2 = 0.0, sR = 0.0, ssq = 0.0;
-    for (long long i = threadIdx.x; i < m; i += kBST) {
+    // ---- folds: rows (chunk order), this CTA's column partials (row-set order)
+    double sr = 0.0, sr2 = 0.0, ssq = 0.0;
+    for (long long i = rb + threadIdx.x; i < re; i += kBST) {
       double R = 0.0;
       for (int c = 0; c < nch; ++c) R += rowp[i * nch + c];
       const double ri = R - p_s[i];
       r_s[i] = ri;
       sr += ri;
       sr2 += ri * ri;
-      sR += R;
     }
     for (long long j = threadIdx.x; j < n; j += kBST) {
       double S = 0.0;
       for (int t = 0; t < nsets; ++t) S += colbuf[(long long)t * ld + j];
+      cpart[j] = S;
+    }
+    {
+      const double t1 = block_sum_n<kBSW>(sr, red);
+      const double t2 = block_sum_n<kBSW>(sr2, red);
+      if (threadIdx.x == 0) {
+        xs[0] = t1;
+        xs[1] = t2;
+      }
+    }
+    if constexpr (CS > 1) cg::this_cluster().sync();  // peers' partials visible (DSMEM)
+    else __syncthreads();
+    // column sums and scalars folded in cluster-rank order (same in every CTA)
+    for (long long j = threadIdx.x; j < n; j += kBST) {
+      double S = 0.0;
+#pragma unroll
+      for (int r = 0; r < CS; ++r) {
+        const double* pc = CS > 1 ? cg::this_cluster().map_shared_rank(cpart, r) : cpart;
+        S += pc[j];
+      }
       const double sj = __dsub_rn(S, q_s[j]);
       s_s[j] = sj;
       ssq += sj * sj;
     }
     {
-      const double t1 = block_sum_n<kBSW>(sr, red);
-      const double t2 = block_sum_n<kBSW>(sr2, red);
       const double t4 = block_sum_n<kBSW>(ssq, red);
-      (void)sR;
       if (threadIdx.x == 0) {
-        bc[0] = t1;
-        bc[1] = t2;
+        double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+        for (int r = 0; r < CS; ++r) {
+          const double* px = CS > 1 ? cg::this_cluster().map_shared_rank(xs, r) : xs;
+          u0 += px[0];
+          u1 += px[1];
+        }
+        bc[0] = u0;
+        bc[1] = u1;
         bc[3] = t4;
       }
     }
     __syncthreads();
     eta = __ddiv_rn(bc[0], mn);
     const double shift = __dsub_rn(2.0 * eta, theta);
-    for (long long i = threadIdx.x; i < m; i += kBST) {
+    for (long long i = rb + threadIdx.x; i < re; i += kBST) {
       const double ri = r_s[i], ai = a_s[i];
       phi_s[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift), dn);
       a_s[i] = __dsub_rn(ai, ri);
@@ -230,9 +264,11 @@ __global__ void __launch_bounds__(NT, 512 / NT) bstream_kernel(BStreamArgs A) {
         term = TERM_MAXITER;
       }
     }
-    __syncthreads();  // phi / psi complete before the next sweep (and bc reuse)
+    // phi / psi complete before the next sweep; peers done reading cpart / xs
+    if constexpr (CS > 1) cg::this_cluster().sync();
+    else __syncthreads();
     if (done) {
-      if (threadIdx.x == 0) {
+      if (threadIdx.x == 0 && crank == 0) {
         ctl->k = k;
         ctl->theta[k & 1] = theta;
         ctl->eta = eta;
@@ -248,8 +284,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) bstream_kernel(BStreamArgs A) {
   // primal objective <C,X> + h(X) (problem.cpp:76-85, regularizers.cpp:49-51)
   {
     double lin = 0.0, xsq = 0.0;
-    for (long long t = threadIdx.x; t < m * (ld / VEC); t += kBST) {
-      const long long i = t / (ld / VEC), cv = t % (ld / VEC);
+    for (long long t = threadIdx.x; t < (re - rb) * (ld / VEC); t += kBST) {
+      const long long i = rb + t / (ld / VEC), cv = t % (ld / VEC);
       double x[VEC], c[VEC];
       unpack(reinterpret_cast<const V*>(Xg + i * ld)[cv], x);
       unpack(reinterpret_cast<const V*>(Cg + i * ld)[cv], c);
@@ -261,18 +297,36 @@ __global__ void __launch_bounds__(NT, 512 / NT) bstream_kernel(BStreamArgs A) {
     }
     const double t1 = block_sum_n<kBSW>(lin, red);
     const double t2 = block_sum_n<kBSW>(xsq, red);
-    if (threadIdx.x == 0) ctl->objective = t1 + (quad ? 0.5 * prm.alpha * t2 : 0.0);
+    if (threadIdx.x == 0) {
+      xs[2] = t1;
+      xs[3] = t2;
+    }
+    if constexpr (CS > 1) cg::this_cluster().sync();
+    else __syncthreads();
+    if (threadIdx.x == 0 && crank == 0) {
+      double u1 = 0.0, u2 = 0.0;
+#pragma unroll
+      for (int r = 0; r < CS; ++r) {
+        const double* px = CS > 1 ? cg::this_cluster().map_shared_rank(xs, r) : xs;
+        u1 += px[2];
+        u2 += px[3];
+      }
+      ctl->objective = u1 + (quad ? 0.5 * prm.alpha * u2 : 0.0);
+    }
   }
-  for (long long i = threadIdx.x; i < m; i += kBST) {
+  for (long long i = rb + threadIdx.x; i < re; i += kBST) {
     A.phi[prob * m + i] = phi_s[i];
     A.a[prob * m + i] = a_s[i];
     A.r[prob * m + i] = r_s[i];
   }
-  for (long long j = threadIdx.x; j < n; j += kBST) {
-    A.psi[prob * n + j] = psi_s[j];
-    A.b[prob * n + j] = b_s[j];
-    A.s[prob * n + j] = s_s[j];
+  if (crank == 0) {
+    for (long long j = threadIdx.x; j < n; j += kBST) {
+      A.psi[prob * n + j] = psi_s[j];
+      A.b[prob * n + j] = b_s[j];
+      A.s[prob * n + j] = s_s[j];
+    }
   }
+  if constexpr (CS > 1) cg::this_cluster().sync();  // no CTA exits while peers read its smem
 }
 
 }  // namespace otdrk

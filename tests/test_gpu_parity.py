@@ -449,12 +449,14 @@ def test_resident_matches_streaming(ora, monkeypatch, storage, m, n, kind):
     assert abs(a[1].objective - b[1].objective) <= (1e-9 if storage == "f64" else 1e-6) * abs(b[1].objective)
 
 
-@pytest.mark.parametrize("mode", ["stream", "resident"])
+@pytest.mark.parametrize("mode", ["stream", "stream1", "resident"])
 @pytest.mark.parametrize("storage", ["f64", "f32"])
 def test_batched_solve_matches_sequential(ora, monkeypatch, storage, mode):
-    """cfg5 shape at reduced batch: one launch (CTA-per-problem streaming, or
-    cluster-resident) == B solve()s."""
-    monkeypatch.setenv("OTDR_BATCH", mode)
+    """cfg5 shape at reduced batch: one launch (streaming with a 2-CTA cluster
+    or one CTA per problem, or cluster-resident) == B solve()s."""
+    monkeypatch.setenv("OTDR_BATCH", "resident" if mode == "resident" else "stream")
+    if mode == "stream1":
+        monkeypatch.setenv("OTDR_BATCH_CLUSTER", "1")
     B, m = 6, 96
     probs = [ora.gaussian_problem(m, m, b) for b in range(B)]
     alpha = 5e-3 * 2 * m
