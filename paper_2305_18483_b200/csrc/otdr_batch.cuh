@@ -102,7 +102,10 @@ struct otdr_batch {
   }
   template <typename T>
   void launch_stream() {
-    if (bs_cs == 2) {
+    if (bs_cs == 4) {
+      if (bs_nt == 512) launch_stream_nt<T, 512, 4>();
+      else launch_stream_nt<T, 256, 4>();
+    } else if (bs_cs == 2) {
       if (bs_nt == 512) launch_stream_nt<T, 512, 2>();
       else launch_stream_nt<T, 256, 2>();
     } else {
@@ -197,7 +200,7 @@ otdr_status otdr_batch_create(int device, otdr_storage storage, int64_t batch, i
       const long long vecw = 32 * (bt->f64() ? 2 : 4);
       const long long nch = (bt->ld + vecw - 1) / vecw;
       if (const char* bn = std::getenv("OTDR_BATCH_THREADS")) bt->bs_nt = std::atoi(bn) == 512 ? 512 : 256;
-      if (const char* bc = std::getenv("OTDR_BATCH_CLUSTER")) bt->bs_cs = std::atoi(bc) == 1 ? 1 : 2;
+      if (const char* bc = std::getenv("OTDR_BATCH_CLUSTER")) bt->bs_cs = std::atoi(bc) == 1 ? 1 : std::atoi(bc) == 4 ? 4 : 2;
       const int nw = bt->bs_nt / 32;
       if (nch <= nw) {
         bt->bs_nch = int(nch);
