@@ -1,10 +1,9 @@
 // otdr_stream.cuh -- persistent streaming solve loop for plans that live in
-// HBM (single GPU, zero / quadratic regularizer).
+// HBM (zero / quadratic regularizer; single GPU or row-sharded).
 //
 // One cooperative launch runs many DR iterations (solver.cpp:95-102 + :23-38):
-// every CTA of a co-resident grid (P = SMs x CTAs/SM) owns a fixed, equal
-// share of the plan for the whole solve, so there are no per-iteration
-// launches, no wave tail and no separate reduce/update kernels.
+// P = SMs x 2 co-resident CTAs sweep the plan every iteration, so there are
+// no per-iteration launches and no separate reduce / update kernels.
 //
 // Work split. The plan is cut into tiles of rows x 256 columns, numbered
 // stripe-major (all row ranges of stripe 0, then stripe 1, ...); the last
@@ -14,20 +13,24 @@
 // 20000^2, dynamic claiming lets fast CTAs take more tiles.
 //
 // One iteration:
-//   A  sweep own segments: X <- prox([((X - rho C) + phi_i) + psi_j]_+),
-//      row partials rowpart[row][stripe] (warp butterfly), column partials per
-//      tile in registers -> fixed-order cross-warp smem sum -> colpart[tile]
-//      (one slot per tile: the fold order does not depend on which CTA swept it)
+//   A  sweep the claimed tiles: X <- prox([((X - rho C) + phi_i) + psi_j]_+)
+//      with every thread streaming its own 16-byte chunks of X, C and phi
+//      through a private cp.async queue; row partials rowpart[row][stripe]
+//      (warp butterfly), per-tile column partials (registers -> fixed-order
+//      cross-warp smem sum -> colpart[tile]: one slot per tile, so the fold
+//      order does not depend on which CTA swept it). The CTA completing a
+//      stripe's last tile folds its column partials (tile order): single GPU
+//      s = S - q and the stripe's sum of s^2; row-sharded: S stored into every
+//      rank's receive buffer (NVLink) while the sweep goes on
 //   -- grid barrier --
-//      the CTA completing a stripe's last tile folds its column partials
-//      (tile order): s = S - q and the stripe's sum of s^2
 //   B  row folds (warp per row, stripe order): r = R - p, partial sums of r,
 //      r^2, R; one (sr, sr2, sR) record per CTA
 //   -- grid barrier --
 //   C  every CTA folds the P records in the same fixed order -> identical eta,
-//      shift, r_primal and stopping decision everywhere; phi/a (thread per
-//      row), psi/b (thread per column); the solve loop's stopping logic
-//      (solver.cpp:179-235)
+//      shift, r_primal and stopping decision everywhere (row-sharded: after
+//      the epoch-flag exchange, folding the ranks' contributions in rank
+//      order); phi/a (thread per row), psi/b (thread per column); the solve
+//      loop's stopping logic (solver.cpp:179-235)
 //   -- grid barrier (only when continuing) --
 // Cross-CTA data (phi, psi, r, partials) is read with ld.global.cg (L2), so
 // no stale L1 line survives a barrier; X and C tiles are owned by one CTA.
@@ -61,7 +64,7 @@ struct StreamArgs {
   long long m, n, ld;
   int stripes, ntiles;
   long long iters;        // raw mode (prm.solving == 0): iterations to run
-  unsigned long long* tstamp;  // optional phase timestamps [kTraceIters][P + 8] (debug)
+  unsigned long long* tstamp;  // optional phase timestamps [kTraceIters][P + 12] (debug)
   // Row-sharded runs: the exchange goes over peer memory (NVLink P2P) inside
   // this kernel. peers[r] = rank r's receive buffer (mapped here), layout
   // [2 parities][nranks][n + 4] doubles then [2][nranks] u64 flags.
