@@ -17,6 +17,8 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:swee
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gl_pipe -s 3 -c 1 \
   -o gpurun_out/gl -f python benchmarks/variants.py cfg3 > gpurun_out/ncu_gl.log 2>&1
 
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gl_stream -s 1 -c 1 \
+  -o gpurun_out/glstream -f python benchmarks/gl_step.py > gpurun_out/ncu_glstream.log 2>&1
 timeout 600 python benchmarks/configs.py cfg1 cfg2 cfg3 cfg4 cfg5 > gpurun_out/configs.log 2>&1
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1
 echo all_done

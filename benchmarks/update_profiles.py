@@ -62,6 +62,14 @@ def main():
         s["algorithmic_GBps"] = 12 * 10000 * 10000 / s["duration"] / 1e9
         raw(os.path.join(OUT, "gl.ncu-rep"), os.path.join(PROF, f"{tag}_gl_pipe_cfg3_raw.csv"))
         json.dump(s, open(os.path.join(PROF, f"{tag}_gl_pipe_cfg3_summary.json"), "w"), indent=1)
+    if os.path.exists(os.path.join(OUT, "glstream.ncu-rep")):
+        s = summ(os.path.join(OUT, "glstream.ncu-rep"))
+        s["workload"] = "cfg3 (10000^2, 10 classes, lambda 1e-3, fp32): ONE gl_stream_kernel launch of 2 DR iterations"
+        s["iterations_in_launch"] = 2
+        s["algorithmic_bytes_per_iteration"] = 12 * 10000 * 10000
+        s["dram_bytes_per_iteration"] = s["dram_bytes"] / 2
+        s["algorithmic_GBps"] = 2 * 12 * 10000 * 10000 / s["duration"] / 1e9
+        json.dump(s, open(os.path.join(PROF, f"{tag}_gl_stream_cfg3_summary.json"), "w"), indent=1)
     for src, dst in (("launches.csv", f"{tag}_launches_20000_f32.csv"), ("configs.log", f"{tag}_configs.jsonl")):
         if os.path.exists(os.path.join(OUT, src)):
             shutil.copy(os.path.join(OUT, src), os.path.join(PROF, dst))
