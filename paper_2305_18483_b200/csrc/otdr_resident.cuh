@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(kRT, 1) resident_kernel(ResidentArgs A) {
   const int nsets = resident_row_sets<T>(ld);
   const long long nch = (ld + 32 * VEC - 1) / (32 * VEC);
   __shared__ double red[kRW];
+  __shared__ double red3[kRW][3];
   __shared__ double bc[4];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -259,9 +260,24 @@ __global__ void __launch_bounds__(kRT, 1) resident_kernel(ResidentArgs A) {
       sR += Rr;
     }
     {
-      const double t1 = block_sum_r(sr, red);
-      const double t2 = block_sum_r(sr2, red);
-      const double t3 = block_sum_r(sR, red);
+      // three fixed-order block sums in one pass (one barrier pair)
+      sr = warp_sum(sr);
+      sr2 = warp_sum(sr2);
+      sR = warp_sum(sR);
+      __syncthreads();
+      if (lane == 0) {
+        red3[warp][0] = sr;
+        red3[warp][1] = sr2;
+        red3[warp][2] = sR;
+      }
+      __syncthreads();
+      double t1 = 0.0, t2 = 0.0, t3 = 0.0;
+      if (threadIdx.x == 0)
+        for (int w = 0; w < kRW; ++w) {
+          t1 += red3[w][0];
+          t2 += red3[w][1];
+          t3 += red3[w][2];
+        }
       if (threadIdx.x == 0) {
         if constexpr (CLUSTER) {
           xrow[n] = t1;
@@ -280,10 +296,14 @@ __global__ void __launch_bounds__(kRT, 1) resident_kernel(ResidentArgs A) {
       }
     }
     xsync();  // ---- 2. column partials and scalar partials visible
-    if (warp < 2) {
-      const double u = warp_fold(n + warp);
-      if (lane == 0) bc[warp] = u;
+    // the scalar folds (last two warps) and each warp's first owned column
+    // fold are in flight together: one L2 round trip before the recurrence
+    if (warp == kRW - 1 || warp == kRW - 2) {
+      const double u = warp_fold(n + (kRW - 1 - warp));
+      if (lane == 0) bc[kRW - 1 - warp] = u;
     }
+    const long long jfirst = j0 + warp;
+    const double Sfirst = jfirst < j1 ? warp_fold(jfirst) : 0.0;
     __syncthreads();
     const double eta = __ddiv_rn(bc[0], mn);
     const double shift = __dsub_rn(2.0 * eta, theta);
@@ -296,8 +316,8 @@ __global__ void __launch_bounds__(kRT, 1) resident_kernel(ResidentArgs A) {
       av[i0 + t] = __dsub_rn(ai, ri);
     }
     double ssq = 0.0;  // warp per owned column: lanes fold the G partials
-    for (long long j = j0 + warp; j < j1; j += kRW) {
-      const double S = warp_fold(j);
+    for (long long j = jfirst; j < j1; j += kRW) {
+      const double S = j == jfirst ? Sfirst : warp_fold(j);
       if (lane == 0) {
         const double sj = __dsub_rn(S, qv[j]);
         const double bj = bv[j];
@@ -327,7 +347,9 @@ __global__ void __launch_bounds__(kRT, 1) resident_kernel(ResidentArgs A) {
         psi_s[j] = xbuf(h)[j];
       }
     } else {
-      for (long long j = threadIdx.x; j < n; j += kRT) psi_s[j] = __ldcg(psi + j);
+      // warp 0 folds the sum s^2 partials while the other warps gather psi
+      if (warp > 0)
+        for (long long j = threadIdx.x - 32; j < n; j += kRT - 32) psi_s[j] = __ldcg(psi + j);
     }
     if (warp == 0) {
       const double u4 = warp_fold(n + 3);
