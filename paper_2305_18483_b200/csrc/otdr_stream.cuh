@@ -537,7 +537,12 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
     stamp(P + 3);
 
     // ---- C. scalar folds (same order in every CTA), recurrence, stopping
+    double pre_r = 0.0, pre_a = 0.0, pre_s = 0.0, pre_b = 0.0;
     if (peer) {
+      if (gtid < m) {  // row operands in flight during the exchange
+        pre_r = __ldcg(A.r + gtid);
+        pre_a = A.a[gtid];
+      }
       // exchange: CTA 0 sends this rank's (sum r, sum r^2, sum R) and the
       // epoch flags; every CTA waits for all ranks, then folds in rank order
       if (c == 0 && warp < 3) {
@@ -576,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
         A.b[j] = __dsub_rn(bj, sj);
       }
       for (long long i = gtid; i < m; i += nthr) {
-        const double ri = __ldcg(A.r + i), ai = A.a[i];
+        const double ri = i == gtid ? pre_r : __ldcg(A.r + i), ai = i == gtid ? pre_a : A.a[i];
         A.phi[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift_p), dn);
         A.a[i] = __dsub_rn(ai, ri);
       }
@@ -590,12 +595,24 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
         if (lane == 0) bc[3] = u;
       }
       __syncthreads();
-    } else if (warp < 3) {
-      const double u = warp_fold_strided(A.part + warp, P, 4);
-      if (lane == 0) bc[warp] = u;
-    } else if (warp == 3) {  // sum s^2: stripe partials in stripe order
-      const double u = warp_fold_strided(A.sspart, A.stripes, 1);
-      if (lane == 0) bc[3] = u;
+    } else {
+      // this thread's first row / column operands are loaded while the
+      // scalar folds are in flight (one L2 round trip for both)
+      if (gtid < m) {
+        pre_r = __ldcg(A.r + gtid);
+        pre_a = A.a[gtid];
+      }
+      if (gtid < n) {
+        pre_s = __ldcg(A.s + gtid);
+        pre_b = A.b[gtid];
+      }
+      if (warp < 3) {
+        const double u = warp_fold_strided(A.part + warp, P, 4);
+        if (lane == 0) bc[warp] = u;
+      } else if (warp == 3) {  // sum s^2: stripe partials in stripe order
+        const double u = warp_fold_strided(A.sspart, A.stripes, 1);
+        if (lane == 0) bc[3] = u;
+      }
     }
     if (!peer) {
       __syncthreads();
@@ -603,12 +620,12 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
       const double eta_l = __ddiv_rn(bc[0], mn);
       const double shift_l = __dsub_rn(2.0 * eta_l, theta);
       for (long long i = gtid; i < m; i += nthr) {
-        const double ri = __ldcg(A.r + i), ai = A.a[i];
+        const double ri = i == gtid ? pre_r : __ldcg(A.r + i), ai = i == gtid ? pre_a : A.a[i];
         A.phi[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift_l), dn);
         A.a[i] = __dsub_rn(ai, ri);
       }
       for (long long j = gtid; j < n; j += nthr) {
-        const double sj = __ldcg(A.s + j), bj = A.b[j];
+        const double sj = j == gtid ? pre_s : __ldcg(A.s + j), bj = j == gtid ? pre_b : A.b[j];
         A.psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift_l), dm);
         A.b[j] = __dsub_rn(bj, sj);
       }
