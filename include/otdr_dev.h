@@ -173,11 +173,13 @@ otdr_status otdr_dev_load_state(otdr_dev* ctx, const double* X, const double* ph
 otdr_status otdr_dev_read_cost_otpb(otdr_dev* ctx, const char* path, const double* p,
                                     const double* q);
 otdr_status otdr_dev_write_plan_otpb(otdr_dev* ctx, const char* path);
-/* iters raw DR steps (no stopping logic), like calling step() iters times. */
+/* iters raw DR steps (no stopping logic), like calling step() iters times;
+ * one persistent launch when the streaming / resident kernels apply. */
 otdr_status otdr_dev_step(otdr_dev* ctx, double rho, int64_t iters);
 /* Runs the solve loop from the current state with the reference's stopping
- * semantics, device-resident (CUDA-graph while loop, no per-iteration host
- * round trip), then evaluates the objective. */
+ * semantics, device-resident (one persistent kernel launch for the whole
+ * loop, or a CUDA-graph while loop for traces; no per-iteration host round
+ * trip), then evaluates the objective. */
 otdr_status otdr_dev_solve(otdr_dev* ctx, const otdr_solve_opts* opts, otdr_solve_result* res);
 /* Any pointer may be NULL. Local rows for X/phi/a/r; full length n for psi/b/s. */
 otdr_status otdr_dev_get_state(otdr_dev* ctx, double* X, double* phi, double* psi, double* a,
@@ -189,8 +191,9 @@ otdr_status otdr_dev_get_trace(otdr_dev* ctx, otdr_trace_row* rows, int64_t cap,
 /* Times `iters` raw steps kernel by kernel with CUDA events on the context
  * stream (diagnostics for the roofline); state advances by iters. */
 otdr_status otdr_dev_profile(otdr_dev* ctx, double rho, int64_t iters, otdr_kernel_times* out);
-/* Device time (CUDA events on the context stream) of `iters` graph-launched
- * raw steps; state advances by iters. */
+/* Device time (CUDA events on the context stream) of `iters` raw steps on the
+ * configured device loop (one persistent launch, or graphs); state advances
+ * by iters. */
 otdr_status otdr_dev_time_steps(otdr_dev* ctx, double rho, int64_t iters, double* ms);
 /* ---------------------------------------------------------------- peers
  * Peer-memory exchange of row-sharded runs: every rank exports a CUDA IPC
