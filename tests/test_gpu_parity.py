@@ -647,6 +647,40 @@ def test_stream_kernel_matches_graph_loop(ora, monkeypatch, storage):
     assert abs(a[1].objective - b[1].objective) <= (1e-9 if storage == "f64" else 1e-6) * abs(b[1].objective)
 
 
+@pytest.mark.parametrize("storage", ["f64", "f32"])
+def test_compressed_plan_is_bitwise_identical(ora, monkeypatch, storage):
+    """X in a generically-compressible HBM allocation (default for plans
+    >= 16 MB; here also split: first 4 MB compressible, rest plain, one
+    contiguous range) gives the same iterates and solve, bit for bit, as a
+    plain cudaMalloc plan -- compression is lossless, only traffic changes."""
+    m, n = 2300, 2100
+    C, p, q, *_ = ora.gaussian_problem(m, n, 12)
+    out = {}
+    for mode, cap in (("off", None), ("x", None), ("x", "0.004")):
+        monkeypatch.setenv("OTDR_RESIDENT", "off")
+        monkeypatch.setenv("OTDR_COMPRESS", mode)
+        if cap:
+            monkeypatch.setenv("OTDR_COMPRESS_GB", cap)
+        else:
+            monkeypatch.delenv("OTDR_COMPRESS_GB", raising=False)
+        eng = otdr.Engine(m, n, storage)
+        eng.set_problem(C, p, q)
+        eng.set_regularizer(otdr.QuadraticReg(5e-3 * (m + n)))
+        eng.set_state()
+        eng.step(otdr.default_stepsize(m, n), 30)
+        st = eng.get_state()
+        eng.set_state()
+        rep = eng.solve(otdr.SolverOptions(tol_primal=1e-5, max_iter=4000, storage=storage))
+        out[(mode, cap)] = (st, rep)
+        eng.close()
+    base = out[("off", None)]
+    for key in (("x", None), ("x", "0.004")):
+        st, rep = out[key]
+        assert np.array_equal(st.X, base[0].X) and np.array_equal(st.phi, base[0].phi), key
+        assert np.array_equal(st.psi, base[0].psi) and st.theta == base[0].theta, key
+        assert rep.iterations == base[1].iterations and rep.objective == base[1].objective, key
+
+
 def _parallel(fns):
     """Run one callable per rank concurrently (ctypes releases the GIL), so
     every rank's exchange kernel is in flight at the same time."""
