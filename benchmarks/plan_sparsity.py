@@ -1,3 +1,5 @@
+"""Plan sparsity along a 20000^2 quadratic solve: fraction of non-zero entries
+and of all-zero 128-byte lines (what generic HBM compression can skip)."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np

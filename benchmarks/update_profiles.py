@@ -29,6 +29,20 @@ def raw(rep, dst):
         subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], stdout=f, check=True)
 
 
+def l2_compression(rep):
+    """L2 generic-compression figures of the memory-workload section."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "details"], capture_output=True, text=True).stdout
+    got = {}
+    for ln in out.splitlines():
+        if "L2 Compression" in ln:
+            parts = ln.split()
+            try:
+                got[" ".join(parts[:-2]) if parts[-2] in ("%", "sector") else " ".join(parts[:-1])] = float(parts[-1].replace(",", ""))
+            except ValueError:
+                pass
+    return got
+
+
 def main():
     tag = sys.argv[1]
     if os.path.exists(os.path.join(OUT, "stream.ncu-rep")):
@@ -44,7 +58,9 @@ def main():
                    "algorithmic_bytes_per_iteration": 12 * 20000 * 20000,
                    "duration_us_ncu": s["duration"] * 1e6, "duration_per_iteration_us_ncu": s["duration"] * 1e6 / it,
                    "dram_throughput_pct_of_ncu_peak": s["dram_throughput_pct"], "registers": s["registers"],
-                   "grid": s["grid"], "stalls": s.get("stalls"), "issue_active_pct": s.get("issue_active_pct")},
+                   "grid": s["grid"], "stalls": s.get("stalls"), "issue_active_pct": s.get("issue_active_pct"),
+                   "x_allocation": "generic-compressible HBM (first 3.2 GB of X; OTDR_COMPRESS)",
+                   "l2_compression": l2_compression(os.path.join(OUT, "stream.ncu-rep"))},
                   open(os.path.join(PROF, "ncu_stream_summary.json"), "w"), indent=1)
     if os.path.exists(os.path.join(OUT, "sweep.ncu-rep")):
         s = summ(os.path.join(OUT, "sweep.ncu-rep"))
