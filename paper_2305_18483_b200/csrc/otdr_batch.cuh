@@ -50,6 +50,8 @@ struct otdr_batch {
   std::string err;
   void* C = nullptr;
   void* X = nullptr;
+  size_t x_vmm = 0;  // mapped size when X is a compressible VMM allocation
+  bool x_comp = false;
   double *p = nullptr, *q = nullptr, *phi = nullptr, *psi = nullptr, *a = nullptr, *b = nullptr,
          *r = nullptr, *s = nullptr;
   otdrk::Ctl* ctl = nullptr;
@@ -62,6 +64,10 @@ struct otdr_batch {
   bool f64() const { return storage == OTDR_STORE_F64; }
 
   void release() {
+    if (x_vmm) {
+      comp_free(X, x_vmm);
+      X = nullptr;
+    }
     void* ptrs[] = {C, X, p, q, phi, psi, a, b, r, s, ctl, prm};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);
@@ -221,7 +227,17 @@ otdr_status otdr_batch_create(int device, otdr_storage storage, int64_t batch, i
     BCK(cudaEventCreate(&bt->ev1));
     const size_t mat = size_t(batch * m * bt->ld) * bt->esz;
     BCK(cudaMalloc(&bt->C, mat));
-    BCK(cudaMalloc(&bt->X, mat));
+    {  // the batch's plans in compressible HBM, as for one engine (otdr_dev.cu)
+      std::string cm = mat >= (size_t(16) << 20) ? "x" : "off";
+      if (const char* e = std::getenv("OTDR_COMPRESS")) cm = e;
+      double cap_gb = 3.2;
+      if (const char* e = std::getenv("OTDR_COMPRESS_GB")) cap_gb = std::atof(e);
+      if (cm.find('x') != std::string::npos)
+        bt->X = comp_malloc(device, mat, std::min(mat, size_t(std::max(0.0, cap_gb) * 1e9)), &bt->x_vmm,
+                            &bt->x_comp);
+      if (!bt->X) bt->x_vmm = 0;
+    }
+    if (!bt->X) BCK(cudaMalloc(&bt->X, mat));
     BCK(cudaMemset(bt->C, 0, mat));
     BCK(cudaMemset(bt->X, 0, mat));
     bt->p = balloc<double>(size_t(batch * m));
