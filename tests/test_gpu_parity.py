@@ -497,6 +497,36 @@ def test_batched_device_cost_and_512(ora, monkeypatch, mode):
         assert abs(reps[b].objective - o.objective) <= 1e-6 * abs(o.objective)
 
 
+def test_batched_compressed_plans_bitwise(ora, monkeypatch):
+    """B = 24 plans of 512^2 fp32 (24 MB, compressible by default; here also a
+    4 MB compressible prefix) give bit-identical plans and reports to plain
+    cudaMalloc plans."""
+    B, m = 24, 512
+    src = np.empty((B, m, 2))
+    tgt = np.empty((B, m, 2))
+    ps = np.full((B, m), 1.0 / m)
+    for b in range(B):
+        *_, s, t = ora.gaussian_problem(m, m, 100 + b)
+        src[b], tgt[b] = s, t
+    out = []
+    for mode, cap in (("off", None), ("x", None), ("x", "0.004")):
+        monkeypatch.setenv("OTDR_COMPRESS", mode)
+        if cap:
+            monkeypatch.setenv("OTDR_COMPRESS_GB", cap)
+        else:
+            monkeypatch.delenv("OTDR_COMPRESS_GB", raising=False)
+        be = otdr.BatchEngine(B, m, m, "f32")
+        be.build_sqdist_costs(src, tgt, ps, ps)
+        be.set_regularizer(otdr.QuadraticReg(5.12))
+        reps = be.solve(otdr.SolverOptions(tol_primal=1e-4, max_iter=20000))
+        out.append(([(r.iterations, r.objective) for r in reps], be.plans()))
+        be.close()
+    for its, (X, phi, psi) in out[1:]:
+        assert its == out[0][0]
+        assert np.array_equal(X, out[0][1][0]) and np.array_equal(phi, out[0][1][1])
+        assert np.array_equal(psi, out[0][1][2])
+
+
 @pytest.mark.parametrize("kind", ["quad", "gl"])
 def test_nccl_exchange_path_single_rank(ora, kind):
     """The row-sharded code path (reduce -> ncclAllReduce -> update, chunked
