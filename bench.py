@@ -57,8 +57,17 @@ METRIC = "DR iterations/s (20000x20000 quadratic RDROT)"
 UNIT = "iterations/s"
 
 
+# Rehearsal of the N > 1 path on ONE GPU (OTDR_BENCH_SHARED_GPU=1 under
+# torchrun): every rank drives cuda:0, torch.distributed runs over gloo and the
+# contexts get no NCCL id (NCCL refuses two ranks on one device), so the row
+# sharding, the in-kernel CUDA-IPC exchange and the max-over-ranks timing run
+# exactly as on N GPUs -- the numbers are not a measurement (the ranks'
+# kernels time-slice one GPU).
+SHARED_GPU = os.environ.get("OTDR_BENCH_SHARED_GPU", "0") == "1"
+
+
 def env_rank():
-    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+    return (int(os.environ.get("RANK", 0)), 0 if SHARED_GPU else int(os.environ.get("LOCAL_RANK", 0)),
             int(os.environ.get("WORLD_SIZE", 1)))
 
 
@@ -150,7 +159,10 @@ def init_dist(world, local_rank):
     import torch.distributed as dist
 
     torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if SHARED_GPU:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     return dist
 
 
@@ -159,7 +171,7 @@ def max_over_ranks(dist, value: float) -> float:
         return value
     import torch
 
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64, device="cpu" if SHARED_GPU else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -167,7 +179,7 @@ def max_over_ranks(dist, value: float) -> float:
 def bcast_nccl_id(dist, rank):
     from paper_2305_18483_b200 import sharding
 
-    return sharding.broadcast_nccl_id(dist, rank)
+    return None if SHARED_GPU else sharding.broadcast_nccl_id(dist, rank)
 
 
 def connect(dist, eng, world):
@@ -285,14 +297,15 @@ def run_ours(args):
     if path == "stream":
         bytes_per_launch = prof["sweep_bytes"] * args.steps
         achieved = bytes_per_launch / (ms * 1e-3) / 1e9
-        tr = ncu_traffic("stream")
+        # the committed ncu capture is of the unsharded plan: no per-band figure
+        tr = ncu_traffic("stream") if world == 1 else None
         roof = {"kernel": "stream_kernel (persistent solve: sweep + partial folds + recurrence, "
                           f"one launch for all {args.steps} timed iterations)",
                 "bytes_per_launch": bytes_per_launch, "launch_ms": ms,
                 "traffic": tr * args.steps if tr else None}
     else:
         achieved = prof["sweep_bytes"] / (prof["sweep_ms"] * 1e-3) / 1e9
-        tr = ncu_traffic("sweep")
+        tr = ncu_traffic("sweep") if world == 1 else None
         roof = {"kernel": "sweep_kernel (fused clamp+prox+row/col partial sums)",
                 "bytes_per_launch": prof["sweep_bytes"], "launch_ms": prof["sweep_ms"],
                 "traffic": tr}
@@ -347,6 +360,8 @@ def run_ours(args):
             "device_loop": path,
             "clocks": clocks,
         }
+        if SHARED_GPU and world > 1:
+            line["rehearsal"] = "OTDR_BENCH_SHARED_GPU: all ranks on cuda:0 over gloo, not a measurement"
         print(json.dumps(line), flush=True)
     eng.close()
     if dist:
