@@ -915,7 +915,9 @@ struct otdr_dev {
 
   // cp.async queue depth (rows in flight per warp, OTDR_STREAM_D); 0 = register-staged sweep
   int str_d = -1;
-  int default_stream_d() const { return f64() ? 3 : 4; }
+  // measured (profiles/r01g_stream_knobs_20000.txt): fp32 3 beats 4 by 0.3 % at
+  // 10000^2..40000^2 and 1.2 % on 2500-row bands; fp64 2 beats 3 by 1.5 %
+  int default_stream_d() const { return f64() ? 2 : 3; }
   template <typename T, int REG, int D>
   static constexpr size_t stream_smem_of() {
     return D > 0 ? otdrk::stream_async_smem<T, sizeof(T) == 8 ? 4 : 2, D>() : 0;
