@@ -251,7 +251,7 @@ struct otdr_dev {
   std::vector<void*> ipc_opened;
   // persistent streaming solve (single GPU, zero / quadratic, HBM-resident plan)
   bool allow_stream = true;
-  int str_P = 0, str_ntiles = 0, str_tpc = 8, str_tail = 4;
+  int str_P = 0, str_ntiles = 0, str_tpc = 0, str_tail = 4;
   size_t str_part_cap = 0;
   double *str_part = nullptr, *str_colpart = nullptr;
   int str_big = 1, str_small = 1, str_head = 0;
@@ -879,8 +879,12 @@ struct otdr_dev {
     // (>= 128 rows: shorter tiles cost more in pipeline fill and partial
     // folds than they gain in balance -- measured at 4000^2)
     const long long min_rows = std::getenv("OTDR_STREAM_MINROWS") ? std::atoll(std::getenv("OTDR_STREAM_MINROWS")) : 128;
+    // str_tpc = 0 (default): 6 long tiles per CTA below 1M tile-rows (cfg2
+    // 10000^2, 5000-row bands: 3.5 % / 2 % faster), 8 above (20000^2 and up;
+    // profiles/r01g_stream_policy.txt)
+    const long long tpc = str_tpc > 0 ? str_tpc : (m_loc * S < 1000000 ? 6 : 8);
     const long long big = std::min<long long>(
-        std::max<long long>(1, m_loc), std::max<long long>(min_rows, (m_loc * S + str_tpc * P - 1) / (str_tpc * P)));
+        std::max<long long>(1, m_loc), std::max<long long>(min_rows, (m_loc * S + tpc * P - 1) / (tpc * P)));
     // short tail tiles: a quarter of a long tile, but >= 96 rows (smaller tiles
     // cost more in per-tile pipeline fill than they save in tail; measured at
     // 10000^2 and 20000^2)
