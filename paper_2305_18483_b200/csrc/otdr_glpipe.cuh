@@ -248,7 +248,7 @@ __device__ __forceinline__ void gl_pipe_items(const GLPipeArgs& A, unsigned* cla
             double s = 0.0;
 #pragma unroll
             for (int u = 0; u < kGLPWarps; ++u) s += redc[u * W + w];
-            A.colpart[(long long)si * A.ld + col] = s;
+            st_hint(A.colpart + (long long)si * A.ld + col, s, policy_evict_last());
           }
         }
       }
@@ -256,7 +256,7 @@ __device__ __forceinline__ void gl_pipe_items(const GLPipeArgs& A, unsigned* cla
     }
     cp_async_wait<0>();
     for (int t = threadIdx.x; t < L; t += kGLPThreads)
-      A.rowpart[(sg.begin + t) * (long long)A.ngroups + gi] = rowacc[t];
+      st_hint(A.rowpart + (sg.begin + t) * (long long)A.ngroups + gi, rowacc[t], policy_evict_last());
     __syncthreads();  // rowacc / phi_s / s_item reused by the next item
   }
 }
