@@ -14,9 +14,10 @@ Workload (BASELINE.json north star, SURVEY §8(d) "headline n = 20000"):
 
 value  : DR iterations/s with C and X resident in HBM (device time, CUDA events,
          max over ranks). Inputs (3.2 GB) exceed the 126 MB L2, so no flush.
-e2e    : the same metric through the public API (otdr.solve on a host fp64
-         Problem in pinned memory): cost upload, the device solve, and the plan
-         download are all inside the timed region.
+e2e    : the same metric through the public API: one solve with the reference's
+         default options (tol 1e-4) per step on a host fp64 problem in ordinary
+         pageable memory -- cost upload, make_state, the device solve and the
+         plan download are all inside the timed region.
 roofline: the dominant kernel against the measured HBM copy bandwidth of
          MEASURED_PEAKS.json, algorithmic bytes 12 B / plan entry / iteration
          (read C, read X, write X). One GPU: the persistent streaming solve
@@ -92,6 +93,84 @@ def ncu_traffic(kernel: str):
     except Exception:
         pass
     return None
+
+
+class DramMeter:
+    """In-run DRAM traffic measurement through NVML GPM (GPU Performance
+    Monitoring, Hopper+): DRAM_BW_UTIL = percent of the DRAM bandwidth NVML
+    considers peak, averaged over the interval between two GPM samples. The
+    unknown NVML denominator is calibrated in the same run against a device
+    copy of known bytes (2 x 2 GiB, the MEASURED_PEAKS.json method), so a
+    kernel's DRAM bytes = its util / the copy's util x the copy's bytes/s x
+    its interval. No profiler, no kernel replay."""
+
+    def __init__(self, index: int):
+        self.ok = False
+        self.err = None
+        try:
+            import pynvml as nv
+
+            self.nv = nv
+            nv.nvmlInit()
+            self.h = self._handle(index)
+            sup = nv.nvmlGpmQueryDeviceSupport(self.h)
+            if not sup.isSupportedDevice:
+                raise RuntimeError("GPM not supported on this device")
+            self.s1 = nv.nvmlGpmSampleAlloc()
+            self.s2 = nv.nvmlGpmSampleAlloc()
+            self.ok = True
+        except Exception as e:  # pragma: no cover - depends on the box
+            self.err = f"{type(e).__name__}: {e}"
+
+    def _handle(self, index):
+        nv = self.nv
+        try:
+            import torch
+
+            pr = torch.cuda.get_device_properties(index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId_v2(bus.encode())
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(index)
+
+    def measure(self, fn):
+        """(DRAM util %, interval s) of running fn() (which must synchronize)."""
+        nv = self.nv
+        nv.nvmlGpmSampleGet(self.h, self.s1)
+        t0 = time.perf_counter()
+        fn()
+        t1 = time.perf_counter()
+        nv.nvmlGpmSampleGet(self.h, self.s2)
+        mg = nv.c_nvmlGpmMetricsGet_t()
+        mg.version = nv.NVML_GPM_METRICS_GET_VERSION
+        mg.numMetrics = 1
+        mg.sample1 = self.s1
+        mg.sample2 = self.s2
+        mg.metrics[0].metricId = nv.NVML_GPM_METRIC_DRAM_BW_UTIL
+        nv.nvmlGpmMetricsGet(mg)
+        return float(mg.metrics[0].value), t1 - t0
+
+    def calibrate(self):
+        """bytes/s that 100 % DRAM_BW_UTIL stands for, from a device copy."""
+        import torch
+
+        n = 1 << 30  # 2 GiB of fp16 per buffer, read + written per copy
+        a = torch.empty(n, dtype=torch.float16, device="cuda")
+        b = torch.empty_like(a)
+        a.fill_(1.0)
+        reps = 40
+
+        def run():
+            for _ in range(reps):
+                b.copy_(a)
+            torch.cuda.synchronize()
+
+        run()
+        util, dt = self.measure(run)
+        del a, b
+        copy_bps = 2.0 * 2 * n * reps / dt
+        self.full_bps = copy_bps / (util / 100.0)
+        return {"copy_GBps": copy_bps / 1e9, "copy_util_pct": util, "interval_s": dt}
 
 
 class ClockSampler:
@@ -209,8 +288,11 @@ def make_engine(rank, world, dist, local_rank):
     return eng
 
 
-def cpu_oracle_rate(iters: int, threads: int):
-    """Times `iters` DR iterations of the oracle on the host; returns (it/s, s/it)."""
+def cpu_oracle_rates(budget_s: float):
+    """The oracle on the host (fp64, the reference's arithmetic): DR
+    iterations/s on all host threads and on ONE thread (the reference build is
+    single-threaded: no OpenMP in proj/CMakeLists.txt), each timed
+    over about `budget_s` seconds of iterations of the full instance."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as ora
 
@@ -219,12 +301,18 @@ def cpu_oracle_rate(iters: int, threads: int):
     st = ora.make_state(pr)
     reg = ora.quad_reg(ALPHA)
     rho = ora.default_stepsize(M, N)
-    ora.step(st, pr, reg, rho, threads=threads)  # warm (page-in)
-    t0 = time.perf_counter()
-    for _ in range(iters):
-        ora.step(st, pr, reg, rho, threads=threads)
-    dt = time.perf_counter() - t0
-    return iters / dt, dt / iters
+    out = {}
+    for threads in (os.cpu_count() or 1, 1):
+        t0 = time.perf_counter()
+        ora.step(st, pr, reg, rho, threads=threads)  # warm (page-in) + rate probe
+        per = time.perf_counter() - t0
+        iters = max(2, int(budget_s / max(per, 1e-3)))
+        t0 = time.perf_counter()
+        for _ in range(iters):
+            ora.step(st, pr, reg, rho, threads=threads)
+        dt = time.perf_counter() - t0
+        out[threads if threads == 1 else "all"] = (iters / dt, dt / iters, iters, threads)
+    return out
 
 
 def run_reference(args):
@@ -322,6 +410,35 @@ def run_ours(args):
                  "graph_path_exchange_ms": prof["exchange_ms"], "graph_path_update_ms": prof["update_ms"],
                  "peak_source": peak_src})
 
+    # in-run DRAM traffic of the same kernel (NVML GPM, calibrated against a
+    # device copy in this run) over a longer launch of the same loop
+    dram = {"source": "unavailable"}
+    meter = DramMeter(local_rank) if torch.cuda.is_available() else None
+    if meter is not None and meter.ok:
+        try:
+            cal = meter.calibrate()
+            km = max(200, int(round(0.25 / max(ms / args.steps * 1e-3, 1e-6))))
+            box = {}
+            util, dt = meter.measure(lambda: box.setdefault("ms", eng.time_steps(rho, km)))
+            dbytes = util / 100.0 * meter.full_bps * dt
+            per_it = dbytes / km
+            dram = {"source": f"NVML GPM DRAM_BW_UTIL over a {km}-iteration launch of the same "
+                              f"kernel in this run, calibrated against a 2 GiB device copy",
+                    "bytes_per_iteration": per_it,
+                    "GBps": dbytes / (box["ms"] * 1e-3) / 1e9, "util_pct": util,
+                    "launch_ms": box["ms"], "calibration": cal}
+        except Exception as e:  # pragma: no cover - depends on the box
+            dram = {"source": f"unavailable ({type(e).__name__}: {e})"}
+    elif meter is not None:
+        dram = {"source": f"unavailable ({meter.err})"}
+    if "bytes_per_iteration" in dram and path == "stream":
+        roof["traffic_ncu_committed"] = roof.get("traffic")
+        roof["traffic"] = dram["bytes_per_iteration"] * args.steps
+        roof["dram_GBps"] = roof["traffic"] / (roof["launch_ms"] * 1e-3) / 1e9
+        roof["dram_frac"] = roof["dram_GBps"] / peak
+        roof["traffic_source"] = "in-run (NVML GPM)"
+    roof["dram_inrun"] = dram
+
     # time to tolerance (device-resident solve loop)
     t_rep = eng.solve(otdr.SolverOptions(tol_primal=1e-4, max_iter=5000, storage="f32"),
                       with_state=False)
@@ -332,12 +449,18 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        rate, spi = cpu_oracle_rate(args.cpu_iters, threads)
+        rates = cpu_oracle_rates(args.cpu_seconds)
+        rate, spi, its, threads = rates["all"]
+        r1, spi1, its1, _ = rates[1]
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{args.cpu_iters} DR iterations of the full 20000x20000 instance "
-                         f"(oracle/otdr_oracle.cpp, {threads} OpenMP threads); time-to-1e-4 "
-                         f"extrapolated {t_rep.iterations * spi:.1f} s"}
+               "nproc": os.cpu_count(),
+               "sample": f"{its} DR iterations of the full 20000x20000 instance "
+                         f"(oracle/otdr_oracle.cpp, fp64, {threads} OpenMP threads); time to 1e-4 "
+                         f"({t_rep.iterations} iterations) extrapolated {t_rep.iterations * spi:.1f} s",
+               "single_thread": {"value": r1, "unit": UNIT, "cores": 1,
+                                 "sample": f"{its1} DR iterations, 1 thread (the reference build is "
+                                           f"single-threaded); time to 1e-4 extrapolated "
+                                           f"{t_rep.iterations * spi1:.1f} s"}}
 
     if rank == 0:
         kpi = eng.kernels_per_iteration()
@@ -382,8 +505,8 @@ def e2e_measure(rank, world, dist, local_rank, args):
 
     lo, hi = shard_rows(rank, world)
     src, tgt = datagen.gaussian_points(M, N, SEED)
-    pin = torch.cuda.is_available()
-    C = torch.empty((hi - lo, N), dtype=torch.float64, pin_memory=pin).numpy()
+    # ordinary (pageable) host memory, as a reference caller's Eigen matrices
+    C = np.empty((hi - lo, N))
     # cost rows of the global normalize_cost(squared_distance_cost) (datagen.cpp:56-65)
     mx = 0.0
     for r0 in range(0, M, 2000):
@@ -393,13 +516,14 @@ def e2e_measure(rank, world, dist, local_rank, args):
         C[r0 - lo:r1 - lo] = datagen.squared_distance_cost(src[r0:r1], tgt) / mx
     p = datagen.uniform(M)[lo:hi].copy()
     q = datagen.uniform(N)
-    plan_host = torch.empty((hi - lo, N), dtype=torch.float64, pin_memory=pin).numpy()
+    plan_host = np.empty((hi - lo, N))
+    plan_host.fill(0.0)  # touch: first-fault page mapping is not transfer time
     shard = otdr.Shard(rank, world, lo, hi, bcast_nccl_id(dist, rank)) if world > 1 else None
     eng = otdr.Engine(M, N, "f32", device=local_rank if world > 1 else 0, shard=shard)
     connect(dist, eng, world)
     reg = otdr.QuadraticReg(ALPHA)
-    iters = args.e2e_iters
-    opts = otdr.SolverOptions(tol_primal=1e-300, max_iter=iters, storage="f32")
+    # the reference's default SolverOptions (solver.hpp:39-49): tol_primal 1e-4
+    opts = otdr.SolverOptions(storage="f32")
     times = []
     for rep in range(3):  # first call instantiates the graphs
         if dist:
@@ -414,11 +538,13 @@ def e2e_measure(rank, world, dist, local_rank, args):
         times.append(max_over_ranks(dist, dt))
     eng.close()
     dt = min(times[1:])
+    iters = int(r.iterations)
     return {"value": iters / dt, "unit": UNIT, "h2d_bytes_per_step": 8 * (hi - lo) * N + 8 * (hi - lo + N),
             "d2h_bytes_per_step": 8 * (hi - lo) * N,
-            "step": f"one public-API solve of {iters} DR iterations: fp64 cost upload from pinned "
-                    f"host memory, make_state, device loop, fp64 plan download",
-            "seconds_per_solve": dt, "iterations": int(r.iterations)}
+            "step": f"one public-API solve with the reference's default options (tol_primal 1e-4: "
+                    f"{iters} DR iterations): fp64 cost upload from pageable host memory, make_state, "
+                    f"device loop, fp64 plan download to pageable host memory",
+            "seconds_per_solve": dt, "iterations": iters, "termination": r.termination.name}
 
 
 def main():
@@ -427,8 +553,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-iters", type=int, default=3)
-    ap.add_argument("--e2e-iters", type=int, default=350)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()

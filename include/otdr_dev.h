@@ -246,6 +246,13 @@ otdr_status otdr_batch_solve(otdr_batch* bt, const otdr_solve_opts* opts,
                              otdr_solve_result* results);
 /* any pointer may be NULL: X B x m x n, phi B x m, psi B x n. */
 otdr_status otdr_batch_get_plans(otdr_batch* bt, double* X, double* phi, double* psi);
+/* The complete final SolverState of every problem (solver.hpp:51-59, owned by
+ * each SolveReport, solver.hpp:74-87) -- what B sequential solve() calls
+ * return. Any pointer may be NULL: X B x m x n; phi, a, r B x m; psi, b, s
+ * B x n; theta, eta, k B entries. */
+otdr_status otdr_batch_get_state(otdr_batch* bt, double* X, double* phi, double* psi, double* a,
+                                 double* b, double* r, double* s, double* theta, double* eta,
+                                 int64_t* k);
 
 #ifdef __cplusplus
 }

@@ -72,7 +72,7 @@ EXPORTS = [
     "otdr_dev_peer_import", "otdr_dev_peer_link_local", "otdr_dev_read_cost_otpb", "otdr_dev_write_plan_otpb",
     "otdr_batch_create", "otdr_batch_destroy", "otdr_batch_last_error", "otdr_batch_set_problems",
     "otdr_batch_build_sqdist_costs", "otdr_batch_set_regularizer", "otdr_batch_solve",
-    "otdr_batch_get_plans",
+    "otdr_batch_get_plans", "otdr_batch_get_state",
     # include/otdr_datagen.h
     "otdr_gaussian_points", "otdr_adaptation_points", "otdr_dev_nccl_unique_id",
 ]
@@ -130,6 +130,8 @@ def lib():
     L.otdr_batch_set_regularizer.argtypes = [vp, ct.c_int, ct.c_double]
     L.otdr_batch_solve.argtypes = [vp, ct.POINTER(SolveOpts), ct.POINTER(SolveResult)]
     L.otdr_batch_get_plans.argtypes = [vp, _dp, _dp, _dp]
+    L.otdr_batch_get_state.argtypes = [vp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
+                                       ct.POINTER(ct.c_int64)]
     L.otdr_dev_kernels_per_iteration.argtypes = [vp]
     L.otdr_dev_kernels_per_iteration.restype = ct.c_int
     L.otdr_dev_solve_path.argtypes = [vp]

@@ -448,4 +448,31 @@ otdr_status otdr_batch_get_plans(otdr_batch* bt, double* X, double* phi, double*
   });
 }
 
+otdr_status otdr_batch_get_state(otdr_batch* bt, double* X, double* phi, double* psi, double* a,
+                                 double* b, double* r, double* s, double* theta, double* eta,
+                                 int64_t* k) {
+  if (!bt) return OTDR_E_INVALID_ARG;
+  const otdr_status st = otdr_batch_get_plans(bt, X, phi, psi);
+  if (st != OTDR_OK) return st;
+  return bguard(bt, [&] {
+    const long long B = bt->B, m = bt->m, n = bt->n;
+    // both batched kernels leave a, r (rows) and b, s (columns) in global memory
+    if (a) BCK(cudaMemcpy(a, bt->a, size_t(B * m) * 8, cudaMemcpyDeviceToHost));
+    if (r) BCK(cudaMemcpy(r, bt->r, size_t(B * m) * 8, cudaMemcpyDeviceToHost));
+    if (b) BCK(cudaMemcpy(b, bt->b, size_t(B * n) * 8, cudaMemcpyDeviceToHost));
+    if (s) BCK(cudaMemcpy(s, bt->s, size_t(B * n) * 8, cudaMemcpyDeviceToHost));
+    if (theta || eta || k) {
+      std::vector<otdrk::Ctl> ctl(static_cast<size_t>(B));
+      BCK(cudaMemcpy(ctl.data(), bt->ctl, ctl.size() * sizeof(otdrk::Ctl), cudaMemcpyDeviceToHost));
+      for (long long pb = 0; pb < B; ++pb) {
+        const otdrk::Ctl& c = ctl[size_t(pb)];
+        if (theta) theta[pb] = c.theta[c.k & 1];
+        if (eta) eta[pb] = c.eta;
+        if (k) k[pb] = c.k;
+      }
+    }
+    return OTDR_OK;
+  });
+}
+
 }  // extern "C"

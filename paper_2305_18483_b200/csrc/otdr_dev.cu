@@ -30,6 +30,7 @@
 #include <map>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -42,6 +43,38 @@ namespace {
 constexpr int kNumSMs = 148;
 constexpr int kSweepTN = 256;  // plain sweep stripe width (both storages)
 constexpr size_t kStageDoubles = size_t(1) << 25;  // 256 MB fp64 staging
+constexpr size_t kPinBytes = size_t(64) << 20;      // pinned host chunk (x2, double-buffered)
+
+// Host threads for the fp64 <-> storage conversions of uploads / downloads
+// (OTDR_HOST_THREADS overrides; the reference API hands us pageable fp64
+// rows, which the DMA engines cannot read directly).
+int host_threads() {
+  static const int t = [] {
+    if (const char* e = std::getenv("OTDR_HOST_THREADS")) return std::max(1, std::atoi(e));
+    const unsigned hc = std::thread::hardware_concurrency();
+    return int(std::min(16u, std::max(1u, hc)));
+  }();
+  return t;
+}
+
+// f(lo, hi) over [0, count) split across the host threads.
+template <typename F>
+void host_parallel(long long count, F&& f) {
+  const int th = host_threads();
+  if (th <= 1 || count < (1LL << 18)) {
+    f(0LL, count);
+    return;
+  }
+  const long long per = (count + th - 1) / th;
+  std::vector<std::thread> pool;
+  pool.reserve(size_t(th));
+  for (int t = 1; t < th; ++t) {
+    const long long lo = t * per, hi = std::min(count, lo + per);
+    if (lo < hi) pool.emplace_back([&f, lo, hi] { f(lo, hi); });
+  }
+  f(0LL, std::min(count, per));
+  for (auto& x : pool) x.join();
+}
 
 struct Error {
   otdr_status code;
@@ -1313,16 +1346,51 @@ struct otdr_dev {
   }
 
   // ---------------------------------------------------------------- upload
+  // Host rows move through two pinned chunks: host threads convert chunk c
+  // (fp64 -> storage type, so fp32 storage crosses PCIe at 4 B/entry) while
+  // the copy engine moves chunk c-1 and a kernel scatters it into the padded,
+  // device-ordered rows. Works the same for pageable and pinned sources.
+  void* hpin[2] = {nullptr, nullptr};
+  cudaEvent_t ev_pin[2] = {nullptr, nullptr};
+  size_t stage_bytes = 0;
+
+  void ensure_pinned() {
+    for (int b = 0; b < 2; ++b) {
+      if (!hpin[b]) CK(cudaHostAlloc(&hpin[b], kPinBytes, cudaHostAllocDefault));
+      if (!ev_pin[b]) {
+        CK(cudaEventCreateWithFlags(&ev_pin[b], cudaEventDisableTiming));
+        CK(cudaEventRecord(ev_pin[b], stream));
+      }
+    }
+  }
+  template <typename T>
+  long long chunk_rows() const {
+    const size_t cap = std::min(kPinBytes, stage_bytes / 2);
+    return std::max<long long>(1, (long long)(cap / (size_t(n) * sizeof(T))));
+  }
+
   template <typename T>
   void upload_rows(T* dst, const double* src_rows) {
     if (m_loc == 0) return;
-    const long long rows_per = std::max<long long>(1, (long long)(kStageDoubles / size_t(n)));
-    for (long long r0 = 0; r0 < m_loc; r0 += rows_per) {
-      const long long rows = std::min(rows_per, m_loc - r0);
-      CK(cudaMemcpyAsync(stage, src_rows + r0 * n, size_t(rows * n) * sizeof(double),
-                         cudaMemcpyHostToDevice, stream));
-      otdrk::scatter_rows_kernel<T><<<4 * kNumSMs, 256, 0, stream>>>(dst, stage, d_dev_row + r0,
-                                                                      rows, n, ld);
+    ensure_pinned();
+    const long long rows_per = chunk_rows<T>();
+    int c = 0;
+    for (long long r0 = 0; r0 < m_loc; r0 += rows_per, ++c) {
+      const int b = c & 1;
+      const long long rows = std::min(rows_per, m_loc - r0), cnt = rows * n;
+      CK(cudaEventSynchronize(ev_pin[b]));  // the DMA of chunk c-2 has left hpin[b]
+      T* hb = static_cast<T*>(hpin[b]);
+      const double* sp = src_rows + r0 * n;
+      host_parallel(cnt, [hb, sp](long long lo, long long hi) {
+        if (sizeof(T) == sizeof(double)) std::memcpy(hb + lo, sp + lo, size_t(hi - lo) * 8);
+        else
+          for (long long t = lo; t < hi; ++t) hb[t] = T(sp[t]);  // round to nearest (= device cvt.rn)
+      });
+      T* db = reinterpret_cast<T*>(reinterpret_cast<char*>(stage) + size_t(b) * (stage_bytes / 2));
+      CK(cudaMemcpyAsync(db, hb, size_t(cnt) * sizeof(T), cudaMemcpyHostToDevice, stream));
+      CK(cudaEventRecord(ev_pin[b], stream));
+      otdrk::scatter_rows_kernel<T, T><<<4 * kNumSMs, 256, 0, stream>>>(dst, db, d_dev_row + r0, rows,
+                                                                        n, ld);
       check_launch();
     }
     CK(cudaStreamSynchronize(stream));
@@ -1331,16 +1399,33 @@ struct otdr_dev {
   template <typename T>
   void download_rows(double* dst_rows, const T* src) {
     if (m_loc == 0) return;
-    const long long rows_per = std::max<long long>(1, (long long)(kStageDoubles / size_t(n)));
-    for (long long r0 = 0; r0 < m_loc; r0 += rows_per) {
-      const long long rows = std::min(rows_per, m_loc - r0);
-      otdrk::gather_rows_kernel<T><<<4 * kNumSMs, 256, 0, stream>>>(stage, src, d_dev_row + r0,
-                                                                     rows, n, ld);
+    ensure_pinned();
+    const long long rows_per = chunk_rows<T>();
+    const long long nch = (m_loc + rows_per - 1) / rows_per;
+    auto enqueue = [&](long long c) {
+      const int b = int(c & 1);
+      const long long r0 = c * rows_per, rows = std::min(rows_per, m_loc - r0);
+      T* db = reinterpret_cast<T*>(reinterpret_cast<char*>(stage) + size_t(b) * (stage_bytes / 2));
+      otdrk::gather_rows_kernel<T, T><<<4 * kNumSMs, 256, 0, stream>>>(db, src, d_dev_row + r0, rows,
+                                                                       n, ld);
       check_launch();
-      CK(cudaMemcpyAsync(dst_rows + r0 * n, stage, size_t(rows * n) * sizeof(double),
-                         cudaMemcpyDeviceToHost, stream));
+      CK(cudaMemcpyAsync(hpin[b], db, size_t(rows * n) * sizeof(T), cudaMemcpyDeviceToHost, stream));
+      CK(cudaEventRecord(ev_pin[b], stream));
+    };
+    enqueue(0);
+    for (long long c = 0; c < nch; ++c) {
+      if (c + 1 < nch) enqueue(c + 1);  // hpin[(c+1)&1] was drained by the host last trip
+      const int b = int(c & 1);
+      CK(cudaEventSynchronize(ev_pin[b]));
+      const long long r0 = c * rows_per, rows = std::min(rows_per, m_loc - r0);
+      const T* hb = static_cast<const T*>(hpin[b]);
+      double* dp = dst_rows + r0 * n;
+      host_parallel(rows * n, [hb, dp](long long lo, long long hi) {
+        if (sizeof(T) == sizeof(double)) std::memcpy(dp + lo, hb + lo, size_t(hi - lo) * 8);
+        else
+          for (long long t = lo; t < hi; ++t) dp[t] = double(hb[t]);
+      });
     }
-    CK(cudaStreamSynchronize(stream));
   }
 
   void upload_vec_rows(double* dst, const double* host_order) {
@@ -1419,6 +1504,10 @@ struct otdr_dev {
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);
     if (h_ctl) cudaFreeHost(h_ctl);
+    for (int b = 0; b < 2; ++b) {
+      if (hpin[b]) cudaFreeHost(hpin[b]);
+      if (ev_pin[b]) cudaEventDestroy(ev_pin[b]);
+    }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
@@ -1648,8 +1737,11 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     ctx->plan_geometry();
     ctx->bpart = dalloc<double>(size_t(ctx->RB + ctx->CB) * 3);
     ctx->csum = dalloc<double>(otdrk::kCertVals);
-    const size_t stage_elems = std::min(kStageDoubles, ml * size_t(ctx->n));
-    ctx->stage = dalloc<double>(std::max<size_t>(stage_elems, size_t(ctx->n)));
+    // two halves (double-buffered transfers), each at least one fp64 row
+    const size_t stage_elems = std::max<size_t>(std::min(kStageDoubles, 2 * ml * size_t(ctx->n)),
+                                                2 * size_t(ctx->n));
+    ctx->stage = dalloc<double>(stage_elems);
+    ctx->stage_bytes = stage_elems * sizeof(double);
     ctx->d_dev_row = dalloc<long long>(ml);
     ctx->dev_row.resize(size_t(ctx->m_loc));
     std::iota(ctx->dev_row.begin(), ctx->dev_row.end(), 0LL);
@@ -2108,7 +2200,13 @@ otdr_status otdr_dev_solve(otdr_dev* ctx, const otdr_solve_opts* o, otdr_solve_r
     ctx->prm.check_every = o->check_every;
     ctx->prm.record_trace = track ? 1 : 0;
     ctx->prm.deterministic = o->deterministic ? 1 : 0;
-    ctx->prm.fused = o->fused ? 1 : 0;
+    // fused even/odd (solver.cpp:127-177) is pinned entry-wise equal to the
+    // unfused loop (test_solver.cpp:342-357). With fp32 storage the even step's
+    // B = X - rho C is an O(rho) quantity whose fp32 rounding grows with the
+    // plan size, and the unfused sweep is also the faster one
+    // once X is compressible -- so fp32 storage runs `fused` on the unfused
+    // kernels; fp64 storage keeps the in-place even/odd buffer.
+    ctx->prm.fused = (o->fused && ctx->f64()) ? 1 : 0;
     ctx->prm.solving = 1;
     if (track) {
       const long long cap = o->max_iter / o->check_every + 2;
@@ -2142,7 +2240,7 @@ otdr_status otdr_dev_solve(otdr_dev* ctx, const otdr_solve_opts* o, otdr_solve_r
     const bool resident = ctx->resident_active(track, cert);
     // tol_gap without a trace runs on the persistent kernels: a launch stops at
     // a check iteration with r_primal <= tol and the certificate kernels decide
-    const bool gap_only = o->has_tol_gap && !track && !o->fused;
+    const bool gap_only = o->has_tol_gap && !track && !ctx->prm.fused;
     const bool pcert = cert && !gap_only;
     const bool gl_streaming = !resident && ctx->gl_stream_active(track, pcert);
     const bool streaming = !resident && (ctx->stream_active(track, pcert) || gl_streaming);

@@ -1797,9 +1797,10 @@ __global__ void unshift_kernel(T* X, const T* C, const Params* prm, long long co
     X[t] = (T)__dadd_rn((double)X[t], __dmul_rn(rho, (double)C[t]));
 }
 
-// Host-order fp64 rows -> device-order storage rows (with the GL permutation).
-template <typename T>
-__global__ void scatter_rows_kernel(T* dst, const double* src, const long long* dev_row,
+// Host-order rows (fp64, or already in the storage type) -> device-order
+// storage rows (with the GL permutation).
+template <typename T, typename S = double>
+__global__ void scatter_rows_kernel(T* dst, const S* src, const long long* dev_row,
                                     long long rows, long long n, long long ld) {
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < rows * n;
        t += (long long)gridDim.x * blockDim.x) {
@@ -1808,14 +1809,14 @@ __global__ void scatter_rows_kernel(T* dst, const double* src, const long long* 
   }
 }
 
-// Device-order storage rows -> host-order fp64 rows.
-template <typename T>
-__global__ void gather_rows_kernel(double* dst, const T* src, const long long* dev_row,
+// Device-order storage rows -> host-order rows (fp64, or the storage type).
+template <typename T, typename S = double>
+__global__ void gather_rows_kernel(S* dst, const T* src, const long long* dev_row,
                                    long long rows, long long n, long long ld) {
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < rows * n;
        t += (long long)gridDim.x * blockDim.x) {
     const long long i = t / n, j = t - i * n;
-    dst[t] = (double)src[dev_row[i] * ld + j];
+    dst[t] = (S)src[dev_row[i] * ld + j];
   }
 }
 

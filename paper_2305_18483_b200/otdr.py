@@ -687,6 +687,22 @@ class BatchEngine:
         self._ck(self._L.otdr_batch_get_plans(self._h, nat.dptr(X), nat.dptr(phi), nat.dptr(psi)))
         return X, phi, psi
 
+    def states(self, with_plan: bool = True) -> list:
+        """Each problem's complete final SolverState (solver.hpp:51-59)."""
+        B, m, n = self.batch, self.m, self.n
+        X = np.empty((B, m, n)) if with_plan else None
+        rows = [np.empty((B, m)) for _ in range(3)]   # phi, a, r
+        cols = [np.empty((B, n)) for _ in range(3)]   # psi, b, s
+        theta, eta = np.empty(B), np.empty(B)
+        k = np.empty(B, dtype=np.int64)
+        self._ck(self._L.otdr_batch_get_state(
+            self._h, nat.dptr(X) if X is not None else None, nat.dptr(rows[0]), nat.dptr(cols[0]),
+            nat.dptr(rows[1]), nat.dptr(cols[1]), nat.dptr(rows[2]), nat.dptr(cols[2]),
+            nat.dptr(theta), nat.dptr(eta), k.ctypes.data_as(ct.POINTER(ct.c_int64))))
+        return [SolverState(X[b] if X is not None else None, rows[0][b], cols[0][b], rows[1][b],
+                            cols[1][b], float(theta[b]), rows[2][b], cols[2][b], float(eta[b]),
+                            int(k[b])) for b in range(B)]
+
 
 def solve_batch(problems, reg: Regularizer, options: Optional[SolverOptions] = None) -> list:
     """`[solve(pr, reg, options) for pr in problems]` for same-shape problems,
@@ -708,10 +724,8 @@ def solve_batch(problems, reg: Regularizer, options: Optional[SolverOptions] = N
                     np.stack([pr.q for pr in problems]))
     be.set_regularizer(reg)
     reps = be.solve(opt)
-    X, phi, psi = be.plans()
-    for b, rep in enumerate(reps):
-        rep.state = SolverState(X[b], phi[b], psi[b], None, None, float("nan"), None, None,
-                                float("nan"), rep.iterations)
+    for rep, st in zip(reps, be.states()):
+        rep.state = st  # the full final state, as solve() returns it (solver.hpp:74-87)
     be.close()
     return reps
 
