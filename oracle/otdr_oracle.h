@@ -16,6 +16,9 @@
  *   src/solver.cpp:15-256             make_state / step / solve / skip count
  *   src/duality.cpp:5-31              recover_duals / duality_gap
  *   tests/support/oracles.cpp:366-380 textbook DR (closed-form affine projection)
+ *   tests/support/oracles.cpp:16-345  affine / polytope projection, projgrad_solve,
+ *                                     LP vertex enumeration, transportation simplex
+ *                                     (otdr_lp_oracles.cpp)
  *
  * All arrays are dense row-major fp64, caller-owned. Status codes equal the
  * product's otdr_status values (include/otdr_dev.h).
@@ -155,6 +158,19 @@ void ora_duality_gap(const ora_problem* pr, const ora_reg* reg, const ora_state*
 /* xs, ys: iters*m*n each. y0: m*n. */
 void ora_dr_reference(const ora_problem* pr, const ora_reg* reg, double rho,
                       const double* y0, int iters, double* xs, double* ys);
+
+/* Algorithm-independent optimality oracles (otdr_lp_oracles.cpp;
+ * tests/support/oracles.cpp:16-345). Dense row-major fp64. */
+void ora_affine_project(int64_t m, int64_t n, const double* Z, const double* p, const double* q,
+                        double* out);
+void ora_polytope_project(int64_t m, int64_t n, const double* Z, const double* p, const double* q,
+                          int max_iter, double tol, double* out);
+int ora_lp_vertex_solve(int64_t m, int64_t n, const double* C, const double* p, const double* q,
+                        double* X, double* value);
+int ora_transport_simplex(int64_t m, int64_t n, const double* C, const double* p,
+                          const double* q, double* X, double* value);
+int ora_projgrad_solve(int64_t m, int64_t n, const double* C, const double* p, const double* q,
+                       double alpha, double* X, double* gm);
 
 #ifdef __cplusplus
 }

@@ -119,6 +119,14 @@ def lib():
                                       ct.c_double, _dp, _dp, _dp]
         L.ora_dr_reference.argtypes = [ct.POINTER(_Problem), ct.POINTER(_Reg), ct.c_double, _dp,
                                        ct.c_int, _dp, _dp]
+        for nm in ("ora_lp_vertex_solve", "ora_transport_simplex"):
+            f = getattr(L, nm)
+            f.restype = ct.c_int
+            f.argtypes = [ct.c_int64, ct.c_int64, _dp, _dp, _dp, _dp, _dp]
+        L.ora_affine_project.argtypes = [ct.c_int64, ct.c_int64, _dp, _dp, _dp, _dp]
+        L.ora_polytope_project.argtypes = [ct.c_int64, ct.c_int64, _dp, _dp, _dp, ct.c_int, ct.c_double, _dp]
+        L.ora_projgrad_solve.restype = ct.c_int
+        L.ora_projgrad_solve.argtypes = [ct.c_int64, ct.c_int64, _dp, _dp, _dp, ct.c_double, _dp, _dp]
         _lib = L
     return _lib
 
@@ -391,3 +399,59 @@ def random_problem(rng: Rng, m: int, n: int, cost_floor: float = 0.0):
     p = p / p.sum()
     q = q / q.sum()
     return validate_problem(C, p, q)
+
+
+# ----------------------------------------------------------------- optimality oracles
+# (tests/support/oracles.cpp:16-345 -- answers that do not come from DR)
+def affine_project(Z, p, q):
+    Z = _f64(Z); p = _f64(p); q = _f64(q)
+    out = np.empty_like(Z)
+    lib().ora_affine_project(Z.shape[0], Z.shape[1], _d(Z), _d(p), _d(q), _d(out))
+    return out
+
+
+def polytope_project(Z, p, q, max_iter=500000, tol=1e-13):
+    Z = _f64(Z); p = _f64(p); q = _f64(q)
+    out = np.empty_like(Z)
+    lib().ora_polytope_project(Z.shape[0], Z.shape[1], _d(Z), _d(p), _d(q), max_iter, tol, _d(out))
+    return out
+
+
+def _lp(fn, C, p, q):
+    C = _f64(C); p = _f64(p); q = _f64(q)
+    X = np.empty_like(C)
+    v = ct.c_double()
+    rc = fn(C.shape[0], C.shape[1], _d(C), _d(p), _d(q), _d(X), ct.byref(v))
+    if rc:
+        raise OracleError(rc, "LP oracle failed")
+    return X, v.value
+
+
+def lp_vertex_solve(C, p, q):
+    """Exact LP by spanning-tree basis enumeration (oracles.cpp:164-211): (plan, value)."""
+    return _lp(lib().ora_lp_vertex_solve, C, p, q)
+
+
+def transport_simplex(C, p, q):
+    """Transportation simplex, Bland's rule (oracles.cpp:213-345): (plan, value)."""
+    return _lp(lib().ora_transport_simplex, C, p, q)
+
+
+def projgrad_solve(C, p, q, alpha):
+    """argmin <C,X> + alpha/2 ||X||^2 over the transport polytope (oracles.cpp:73-101)."""
+    C = _f64(C); p = _f64(p); q = _f64(q)
+    X = np.empty_like(C)
+    gm = ct.c_double()
+    rc = lib().ora_projgrad_solve(C.shape[0], C.shape[1], _d(C), _d(p), _d(q), float(alpha), _d(X),
+                                  ct.byref(gm))
+    if rc:
+        raise OracleError(rc, f"projgrad_solve: gradient mapping {gm.value}")
+    return X
+
+
+def small_suite_problem(sd: int):
+    """acceptance_main.cpp:33-38: seeds 2000+sd, sides 2..4 drawn from the rng."""
+    rng = Rng(2000 + sd)
+    m = 2 + int(rng.uniform01() * 3.0)
+    n = 2 + int(rng.uniform01() * 3.0)
+    return random_problem(rng, m, n)

@@ -12,6 +12,7 @@
 #include "otdr_stream.cuh"
 #include "otdr_glpipe.cuh"
 #include "otdr_bstream.cuh"
+#include "otdr_tstream.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -288,6 +289,12 @@ struct otdr_dev {
   size_t str_part_cap = 0;
   double *str_part = nullptr, *str_colpart = nullptr;
   int str_big = 1, str_small = 1, str_head = 0;
+  // streaming kernel: 1 = TMA producer warp + consumer warps (tstream_kernel,
+  // default), 0 = per-thread cp.async queues (stream_kernel;
+  // OTDR_STREAM_KERNEL=async); ts_cfg picks the consumer geometry
+  int str_kind = 1, ts_cfg = 0;
+  CUtensorMap ts_mapX{}, ts_mapC{};
+  bool ts_maps = false;
   int* d_sfirst = nullptr;
   unsigned* d_scnt = nullptr;
   double* str_sspart = nullptr;
@@ -899,7 +906,8 @@ struct otdr_dev {
     int occ = 0;
     if (str_d < 0) str_d = default_stream_d();
     cudaLaunchConfig_t lc{};
-    stream_dispatch(lc, otdrk::StreamArgs{}, &occ);
+    if (use_tstream()) tstream_dispatch(lc, otdrk::StreamArgs{}, &occ);
+    else stream_dispatch(lc, otdrk::StreamArgs{}, &occ);
     if (occ < 1) return;
     long long P = (long long)num_sms * occ;
     // OTDR_STREAM_GRID caps the persistent grid (several ranks' kernels
@@ -932,8 +940,21 @@ struct otdr_dev {
       ntiles += (m_loc + R - 1) / R;
     }
     first.push_back(int(ntiles));
-    str_big = int(big);
-    str_small = int(small);
+    // TMA kernel: tiles are whole blocks of ts_rb() rows (a block never
+    // straddles two tiles, and phi block copies stay 16-byte aligned)
+    const long long rb = use_tstream() ? ts_rb() : 1;
+    str_big = int((big + rb - 1) / rb * rb);
+    str_small = int((small + rb - 1) / rb * rb);
+    if (rb > 1) {
+      first.clear();
+      ntiles = 0;
+      for (long long st = 0; st < S; ++st) {
+        first.push_back(int(ntiles));
+        const long long R = st >= S - tail_stripes ? str_small : str_big;
+        ntiles += (m_loc + R - 1) / R;
+      }
+      first.push_back(int(ntiles));
+    }
     str_head = int(S - tail_stripes);
     for (void* ptr : {(void*)str_part, (void*)str_colpart, (void*)d_sfirst,
                       (void*)d_scnt, (void*)str_sspart})
@@ -994,6 +1015,48 @@ struct otdr_dev {
     }
   }
 
+  // ---- TMA-producer streaming kernel (otdr_tstream.cuh)
+  // geometry (consumer warps, rows per block, ring stages): fp32 8/16/5,
+  // fp64 8/8/5 (~187 KB of shared memory, one CTA per SM); OTDR_TS_CFG=1
+  // selects 16 consumer warps
+  int ts_rb() const { return ts_cfg == 1 ? 16 : 8; }
+  template <typename T, int REG, int NCW, int RB, int S, int MINB>
+  void tstream_call(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
+    constexpr bool E = sizeof(T) == 8;
+    auto kern = otdrk::tstream_kernel<T, REG, E, NCW, RB, S, MINB>;
+    constexpr size_t smem = otdrk::TSLayout<T, NCW, RB, S>::kBytes;
+    constexpr int nt = (NCW + 1) * 32;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    if (occ) {
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, nt, smem));
+      return;
+    }
+    if (!ts_maps) {
+      encode_map(&ts_mapX, X, otdrk::kStreamTN, RB);
+      encode_map(&ts_mapC, C, otdrk::kStreamTN, RB);
+      ts_maps = true;
+    }
+    lc.blockDim = dim3(unsigned(nt), 1, 1);
+    lc.dynamicSmemBytes = smem;
+    CK(cudaLaunchKernelEx(&lc, kern, sa, ts_mapX, ts_mapC));
+  }
+  template <typename T, int REG>
+  void tstream_dispatch_t(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
+    // fp32: two CTAs per SM of 8 consumer warps (one row per warp per block)
+    // + a producer warp, 5-stage ring of 8-row blocks (~106 KB per CTA);
+    // OTDR_TS_CFG=1: one CTA of 16 consumer warps, 16-row blocks
+    if (ts_cfg == 1) tstream_call<T, REG, 16, 16, 5, 1>(lc, sa, occ);
+    else tstream_call<T, REG, 8, 8, 5, 2>(lc, sa, occ);
+  }
+  void tstream_dispatch(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
+    const bool quad = reg_kind == OTDR_REG_QUAD;
+    if (quad) tstream_dispatch_t<float, otdrk::REG_QUAD>(lc, sa, occ);
+    else tstream_dispatch_t<float, otdrk::REG_NONE>(lc, sa, occ);
+  }
+  // the TMA kernel covers fp32 storage; fp64 rows (2 KB per 256 columns)
+  // keep the per-thread cp.async kernel
+  bool use_tstream() const { return str_kind == 1 && !f64(); }
+
   bool stream_active(bool track, bool cert) const {
     return str_P > 0 && res_G == 0 && !track && !cert && (!prm.fused || str_d > 0);
   }
@@ -1023,7 +1086,8 @@ struct otdr_dev {
     attr[0].val.cooperative = 1;
     lc.attrs = attr;
     lc.numAttrs = 1;
-    stream_dispatch(lc, sa, nullptr);
+    if (use_tstream()) tstream_dispatch(lc, sa, nullptr);
+    else stream_dispatch(lc, sa, nullptr);
     if (trace) {  // debug: per-iteration phase times of the first iterations
       std::vector<unsigned long long> h(tsn);
       CK(cudaStreamSynchronize(stream));
@@ -1701,11 +1765,18 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     CK(cudaMemset(ctx->X, 0, mat));
     const size_t ml = size_t(std::max<long long>(ctx->m_loc, 1));
     ctx->p = dalloc<double>(ml);
-    ctx->phi = dalloc<double>(ml + 1);  // +1: 16-byte cp.async of phi pairs
+    ctx->phi = dalloc<double>(ml + 64);  // padding: 16-byte cp.async of phi pairs, block bulk copies
     ctx->a = dalloc<double>(ml);
     ctx->r = dalloc<double>(ml);
     ctx->q = dalloc<double>(size_t(ctx->ld));
-    ctx->psi = dalloc<double>(size_t(ctx->ld));
+    // whole 256-column stripes (bulk copies of a stripe's psi)
+    const size_t psi_cap = size_t((ctx->ld + otdrk::kStreamTN - 1) / otdrk::kStreamTN * otdrk::kStreamTN);
+    ctx->psi = dalloc<double>(psi_cap);
+    {  // -inf everywhere: columns beyond n (and beyond ld, read by the TMA
+       // kernel's stripe copies) clamp to exactly 0
+      const std::vector<double> ninf(psi_cap, -std::numeric_limits<double>::infinity());
+      CK(cudaMemcpy(ctx->psi, ninf.data(), psi_cap * 8, cudaMemcpyHostToDevice));
+    }
     ctx->b = dalloc<double>(size_t(ctx->ld));
     ctx->s = dalloc<double>(size_t(ctx->ld));
     CK(cudaMemset(ctx->q, 0, size_t(ctx->ld) * 8));
@@ -1722,6 +1793,8 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     if (const char* tp = std::getenv("OTDR_STREAM_TILES")) ctx->str_tpc = std::max(1, std::atoi(tp));
     if (const char* tl = std::getenv("OTDR_STREAM_TAIL")) ctx->str_tail = std::max(1, std::atoi(tl));
     if (const char* sd = std::getenv("OTDR_STREAM_D")) ctx->str_d = std::atoi(sd);
+    if (const char* sk = std::getenv("OTDR_STREAM_KERNEL")) ctx->str_kind = std::strcmp(sk, "async") == 0 ? 0 : 1;
+    if (const char* tc = std::getenv("OTDR_TS_CFG")) ctx->ts_cfg = std::atoi(tc);
     {
       int occ = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, otdrk::finalize_kernel,

@@ -84,6 +84,7 @@ struct Ctl {
   unsigned int gl_done;        //   CTAs finished (the last one resets both)
   unsigned int pad_;
   unsigned long long bar_gls;  // persistent group-lasso solve kernel
+  unsigned long long bar_tst;  // TMA-producer streaming solve kernel
 };
 
 struct TraceRow {

@@ -414,6 +414,230 @@ __device__ __forceinline__ void stream_stripe_done(const StreamArgs& A, long lon
   }
 }
 
+
+// Loop state of a persistent streaming solve (identical in every CTA).
+struct StreamLoop {
+  long long k, last_imp, k0, it;
+  double theta, best;
+  unsigned long long epoch;
+  int shifted;
+};
+
+// Phases B and C of one DR iteration of the persistent streaming kernels,
+// after the sweep (phase A) of every CTA: grid barrier, row folds, scalar
+// folds (fixed order: every CTA derives the same eta, shift, r_primal and
+// stopping decision), the recurrence (solver.cpp:23-38) and the solve loop's
+// stopping logic (solver.cpp:179-235). NT threads per CTA, all of which call
+// this. Returns true when the launch ends (state written to ctl).
+template <int NT, typename Stamp>
+__device__ __forceinline__ bool stream_finish_iteration(const StreamArgs& A, const Params& prm,
+                                                        StreamLoop& L, double* sred, double* bc,
+                                                        unsigned long long* bar, Stamp&& stamp) {
+  Ctl* ctl = A.ctl;
+  const int c = (int)blockIdx.x, P = (int)gridDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long m = A.m, n = A.n;
+  const long long gwarp = (long long)c * (NT / 32) + warp, nwarps = (long long)P * (NT / 32);
+  const long long gtid = (long long)c * NT + threadIdx.x, nthr = (long long)P * NT;
+  const double dm = (double)A.m_glob, dn = (double)n, mn = (double)(A.m_glob + n);
+  const long long k0 = L.k0;
+  const bool peer = A.peers != nullptr;
+    grid_barrier(bar);
+    stamp(P + 1);
+
+    // ---- B. row folds (warp per row, stripe order) and column folds (CTA order)
+    double sr = 0.0, sr2 = 0.0, sR = 0.0;
+    for (long long i0 = gwarp * 4; i0 < m; i0 += nwarps * 4) {  // 4 rows per warp trip
+      double R[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int t = lane; t < A.stripes; t += 32) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i0 + u < m) R[u] += __ldcg(A.rowpart + (i0 + u) * A.stripes + t);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        R[u] = warp_sum(R[u]);
+        if (lane == 0 && i0 + u < m) {
+          const double ri = R[u] - A.p[i0 + u];
+          A.r[i0 + u] = ri;
+          sr += ri;
+          sr2 += ri * ri;
+          sR += R[u];
+        }
+      }
+    }
+    stamp(P + 5);
+    stamp(P + 6);
+    {
+      const double t1 = block_sum_n<NT / 32>(sr, sred);
+      const double t2 = block_sum_n<NT / 32>(sr2, sred);
+      const double t3 = block_sum_n<NT / 32>(sR, sred);
+      if (threadIdx.x == 0) {
+        A.part[c * 4 + 0] = t1;
+        A.part[c * 4 + 1] = t2;
+        A.part[c * 4 + 2] = t3;
+      }
+    }
+    stamp(P + 2);
+    grid_barrier(bar);
+    stamp(P + 3);
+
+    // ---- C. scalar folds (same order in every CTA), recurrence, stopping
+    double pre_r = 0.0, pre_a = 0.0, pre_s = 0.0, pre_b = 0.0;
+    if (peer) {
+      if (gtid < m) {  // row operands in flight during the exchange
+        pre_r = __ldcg(A.r + gtid);
+        pre_a = A.a[gtid];
+      }
+      // exchange: CTA 0 sends this rank's (sum r, sum r^2, sum R) and the
+      // L.epoch flags; every CTA waits for all ranks, then folds in rank order
+      if (c == 0 && warp < 3) {
+        const double u = warp_fold_strided(A.part + warp, P, 4);
+        if (lane == 0)
+          for (int r = 0; r < A.nranks; ++r)
+            xslot(A.peers[r], int(L.epoch & 1), A.rank, A.nranks, n)[n + warp] = u;
+      }
+      if (c == 0) {
+        __syncthreads();
+        if (threadIdx.x == 0) xpublish(A.peers, A.rank, A.nranks, n, L.epoch);
+      }
+      stamp(P + 8);
+      if (threadIdx.x == 0) xwait(A.rbuf, A.nranks, n, L.epoch);
+      __syncthreads();
+      stamp(P + 9);
+      if (warp < 3) {
+        double u = 0.0;
+        if (lane == 0)
+          for (int r = 0; r < A.nranks; ++r)
+            u += __ldcg(xslot(A.rbuf, int(L.epoch & 1), r, A.nranks, n) + n + warp);
+        if (lane == 0) bc[warp] = u;
+      }
+      __syncthreads();
+      if (c == 0 && threadIdx.x == 0) ctl->tile_ctr = 0;
+      const double eta_p = __ddiv_rn(bc[0], mn);
+      const double shift_p = __dsub_rn(2.0 * eta_p, L.theta);
+      double ssq = 0.0;
+      for (long long j = gtid; j < n; j += nthr) {
+        double S = 0.0;
+        for (int r = 0; r < A.nranks; ++r) S += __ldcg(xslot(A.rbuf, int(L.epoch & 1), r, A.nranks, n) + j);
+        const double sj = __dsub_rn(S, A.q[j]), bj = A.b[j];
+        A.s[j] = sj;
+        ssq += sj * sj;
+        A.psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift_p), dm);
+        A.b[j] = __dsub_rn(bj, sj);
+      }
+      for (long long i = gtid; i < m; i += nthr) {
+        const double ri = i == gtid ? pre_r : __ldcg(A.r + i), ai = i == gtid ? pre_a : A.a[i];
+        A.phi[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift_p), dn);
+        A.a[i] = __dsub_rn(ai, ri);
+      }
+      const double t4 = block_sum_n<NT / 32>(ssq, sred);
+      if (threadIdx.x == 0) A.part[c * 4 + 3] = t4;
+      stamp(P + 10);
+      grid_barrier(bar);  // phi / psi / s complete, ssq partials visible
+      stamp(P + 11);
+      if (warp == 0) {
+        const double u = warp_fold_strided(A.part + 3, P, 4);
+        if (lane == 0) bc[3] = u;
+      }
+      __syncthreads();
+    } else {
+      // this thread's first row / column operands are loaded while the
+      // scalar folds are in flight (one L2 round trip for both)
+      if (gtid < m) {
+        pre_r = __ldcg(A.r + gtid);
+        pre_a = A.a[gtid];
+      }
+      if (gtid < n) {
+        pre_s = __ldcg(A.s + gtid);
+        pre_b = A.b[gtid];
+      }
+      if (warp < 3) {
+        const double u = warp_fold_strided(A.part + warp, P, 4);
+        if (lane == 0) bc[warp] = u;
+      } else if (warp == 3) {  // sum s^2: stripe partials in stripe order
+        const double u = warp_fold_strided(A.sspart, A.stripes, 1);
+        if (lane == 0) bc[3] = u;
+      }
+    }
+    if (!peer) {
+      __syncthreads();
+      if (c == 0 && threadIdx.x == 0) ctl->tile_ctr = 0;  // every CTA is past its last claim
+      const double eta_l = __ddiv_rn(bc[0], mn);
+      const double shift_l = __dsub_rn(2.0 * eta_l, L.theta);
+      for (long long i = gtid; i < m; i += nthr) {
+        const double ri = i == gtid ? pre_r : __ldcg(A.r + i), ai = i == gtid ? pre_a : A.a[i];
+        A.phi[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift_l), dn);
+        A.a[i] = __dsub_rn(ai, ri);
+      }
+      for (long long j = gtid; j < n; j += nthr) {
+        const double sj = j == gtid ? pre_s : __ldcg(A.s + j), bj = j == gtid ? pre_b : A.b[j];
+        A.psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift_l), dm);
+        A.b[j] = __dsub_rn(bj, sj);
+      }
+    }
+    const double eta = __ddiv_rn(bc[0], mn);
+    stamp(P + 4);
+    const double nr2 = sqrt(bc[1]), ns2 = sqrt(bc[3]);
+    const double rp = (nr2 < ns2) ? ns2 : nr2;  // std::max semantics (solver.cpp:179)
+    L.theta = __dsub_rn(L.theta, eta);
+    ++L.k;
+    ++L.it;
+    ++L.epoch;
+    if (prm.fused) L.shifted ^= 1;
+    const long long kk = L.k - k0;
+    bool done = false, want_cert = false;
+    int term = TERM_MAXITER;
+    if (prm.solving) {
+      if (!(rp - rp == 0.0)) {  // solver.cpp:181-185
+        done = true;
+        term = TERM_NONFINITE;
+      } else {
+        if (rp < L.best * (1.0 - 1e-14)) {  // solver.cpp:200-203
+          L.best = rp;
+          L.last_imp = kk;
+        }
+        const bool at_check = (kk % prm.check_every) == 0;
+        if (at_check && rp <= prm.tol_primal && prm.has_tol_gap) {
+          // tol_gap: the launch ends here; the host runs the certificate
+          // kernels, whose finisher applies converged / stalled / max_iter
+          want_cert = true;
+        } else if (at_check && rp <= prm.tol_primal) {
+          done = true;
+          term = TERM_CONVERGED;
+        } else if (kk - L.last_imp >= 10000) {  // solver.cpp:17, :232-235
+          done = true;
+          term = TERM_STALLED;
+        } else if (kk >= prm.max_iter) {
+          done = true;
+          term = TERM_MAXITER;
+        }
+      }
+    } else if (L.it >= A.iters) {
+      done = true;
+    }
+    if (done || want_cert) {
+      if (c == 0 && threadIdx.x == 0) {
+        ctl->k = L.k;
+        ctl->theta[L.k & 1] = L.theta;
+        ctl->eta = eta;
+        ctl->r_primal = rp;
+        ctl->best = L.best;
+        ctl->last_improvement = L.last_imp;
+        ctl->want_cert = want_cert ? 1 : 0;
+        if (prm.solving && done) {
+          ctl->done = 1;
+          ctl->termination = term;
+        }
+        ctl->fused_shifted = L.shifted;
+        if (peer) *A.xep = L.epoch - 1;  // every CTA read the base at entry
+      }
+      return true;
+    }
+    if (!peer) grid_barrier(bar);  // phi / psi complete before the next sweep
+  return false;
+}
+
 template <typename T, int REG, bool EXACT, int NV, int U, int D>
 __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
   Ctl* ctl = A.ctl;
@@ -426,35 +650,30 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
   __shared__ double sred[kWarps];
   __shared__ double bc[4];
   const int c = (int)blockIdx.x, P = (int)gridDim.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long m = A.m, n = A.n;
   __shared__ unsigned s_tile;
   __shared__ bool s_last;
-  const long long gwarp = (long long)c * kWarps + warp, nwarps = (long long)P * kWarps;
-  const long long gtid = (long long)c * kThreads + threadIdx.x, nthr = (long long)P * kThreads;
 
   const double rho = prm.rho, qd = prm.quad_d, qinv = prm.quad_inv;
-  const double dm = (double)A.m_glob, dn = (double)n, mn = (double)(A.m_glob + n);
-  long long k = ctl->k;
-  double theta = ctl->theta[k & 1];
-  double best = ctl->best;
-  long long last_imp = ctl->last_improvement;
-  const long long k0 = ctl->k0;
-  long long it = 0;
-  const bool peer = A.peers != nullptr;
-  const unsigned long long ebase = peer ? *A.xep : 0ull;
-  unsigned long long epoch = ebase + 1;
+  StreamLoop L;
+  L.k = ctl->k;
+  L.theta = ctl->theta[L.k & 1];
+  L.best = ctl->best;
+  L.last_imp = ctl->last_improvement;
+  L.k0 = ctl->k0;
+  L.it = 0;
+  L.epoch = (A.peers != nullptr ? *A.xep : 0ull) + 1;
   // fused even/odd path (solver.cpp:127-177): the X buffer alternates
   // between X (even iterations read C) and B = X - rho C (odd ones do not)
-  int shifted = prm.fused ? ctl->fused_shifted : 0;
+  L.shifted = prm.fused ? ctl->fused_shifted : 0;
+  const long long m = A.m;
 
   auto stamp = [&](int slot) {
-    if (A.tstamp && it < kTraceIters && threadIdx.x == 0 && (slot < P ? true : c == 0))
-      A.tstamp[it * (P + 12) + slot] = globaltimer_ns();
+    if (A.tstamp && L.it < kTraceIters && threadIdx.x == 0 && (slot < P ? true : c == 0))
+      A.tstamp[L.it * (P + 12) + slot] = globaltimer_ns();
   };
   for (;;) {
     stamp(P + 0);
-    const int fmode = prm.fused ? (shifted ? MODE_ODD : MODE_EVEN) : MODE_NORMAL;
+    const int fmode = prm.fused ? (L.shifted ? MODE_ODD : MODE_EVEN) : MODE_NORMAL;
     // ---- A. sweep tiles claimed from the iteration's tile counter
     for (;;) {
       if (threadIdx.x == 0) s_tile = atomicAdd(&ctl->tile_ctr, 1u);
@@ -491,202 +710,10 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
       } else {
         stream_segment<T, REG, EXACT, NV, U>(A, tile, tl.x, tl.y, tl.z, rho, qd, qinv, red);
       }
-      stream_stripe_done(A, tl.x, sred, &s_last, int(epoch & 1));
+      stream_stripe_done(A, tl.x, sred, &s_last, int(L.epoch & 1));
     }
     stamp(c);
-    grid_barrier(&ctl->bar_str);
-    stamp(P + 1);
-
-    // ---- B. row folds (warp per row, stripe order) and column folds (CTA order)
-    double sr = 0.0, sr2 = 0.0, sR = 0.0;
-    for (long long i0 = gwarp * 4; i0 < m; i0 += nwarps * 4) {  // 4 rows per warp trip
-      double R[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int t = lane; t < A.stripes; t += 32) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (i0 + u < m) R[u] += __ldcg(A.rowpart + (i0 + u) * A.stripes + t);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        R[u] = warp_sum(R[u]);
-        if (lane == 0 && i0 + u < m) {
-          const double ri = R[u] - A.p[i0 + u];
-          A.r[i0 + u] = ri;
-          sr += ri;
-          sr2 += ri * ri;
-          sR += R[u];
-        }
-      }
-    }
-    stamp(P + 5);
-    stamp(P + 6);
-    {
-      const double t1 = block_sum(sr, sred);
-      const double t2 = block_sum(sr2, sred);
-      const double t3 = block_sum(sR, sred);
-      if (threadIdx.x == 0) {
-        A.part[c * 4 + 0] = t1;
-        A.part[c * 4 + 1] = t2;
-        A.part[c * 4 + 2] = t3;
-      }
-    }
-    stamp(P + 2);
-    grid_barrier(&ctl->bar_str);
-    stamp(P + 3);
-
-    // ---- C. scalar folds (same order in every CTA), recurrence, stopping
-    double pre_r = 0.0, pre_a = 0.0, pre_s = 0.0, pre_b = 0.0;
-    if (peer) {
-      if (gtid < m) {  // row operands in flight during the exchange
-        pre_r = __ldcg(A.r + gtid);
-        pre_a = A.a[gtid];
-      }
-      // exchange: CTA 0 sends this rank's (sum r, sum r^2, sum R) and the
-      // epoch flags; every CTA waits for all ranks, then folds in rank order
-      if (c == 0 && warp < 3) {
-        const double u = warp_fold_strided(A.part + warp, P, 4);
-        if (lane == 0)
-          for (int r = 0; r < A.nranks; ++r)
-            xslot(A.peers[r], int(epoch & 1), A.rank, A.nranks, n)[n + warp] = u;
-      }
-      if (c == 0) {
-        __syncthreads();
-        if (threadIdx.x == 0) xpublish(A.peers, A.rank, A.nranks, n, epoch);
-      }
-      stamp(P + 8);
-      if (threadIdx.x == 0) xwait(A.rbuf, A.nranks, n, epoch);
-      __syncthreads();
-      stamp(P + 9);
-      if (warp < 3) {
-        double u = 0.0;
-        if (lane == 0)
-          for (int r = 0; r < A.nranks; ++r)
-            u += __ldcg(xslot(A.rbuf, int(epoch & 1), r, A.nranks, n) + n + warp);
-        if (lane == 0) bc[warp] = u;
-      }
-      __syncthreads();
-      if (c == 0 && threadIdx.x == 0) ctl->tile_ctr = 0;
-      const double eta_p = __ddiv_rn(bc[0], mn);
-      const double shift_p = __dsub_rn(2.0 * eta_p, theta);
-      double ssq = 0.0;
-      for (long long j = gtid; j < n; j += nthr) {
-        double S = 0.0;
-        for (int r = 0; r < A.nranks; ++r) S += __ldcg(xslot(A.rbuf, int(epoch & 1), r, A.nranks, n) + j);
-        const double sj = __dsub_rn(S, A.q[j]), bj = A.b[j];
-        A.s[j] = sj;
-        ssq += sj * sj;
-        A.psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift_p), dm);
-        A.b[j] = __dsub_rn(bj, sj);
-      }
-      for (long long i = gtid; i < m; i += nthr) {
-        const double ri = i == gtid ? pre_r : __ldcg(A.r + i), ai = i == gtid ? pre_a : A.a[i];
-        A.phi[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift_p), dn);
-        A.a[i] = __dsub_rn(ai, ri);
-      }
-      const double t4 = block_sum(ssq, sred);
-      if (threadIdx.x == 0) A.part[c * 4 + 3] = t4;
-      stamp(P + 10);
-      grid_barrier(&ctl->bar_str);  // phi / psi / s complete, ssq partials visible
-      stamp(P + 11);
-      if (warp == 0) {
-        const double u = warp_fold_strided(A.part + 3, P, 4);
-        if (lane == 0) bc[3] = u;
-      }
-      __syncthreads();
-    } else {
-      // this thread's first row / column operands are loaded while the
-      // scalar folds are in flight (one L2 round trip for both)
-      if (gtid < m) {
-        pre_r = __ldcg(A.r + gtid);
-        pre_a = A.a[gtid];
-      }
-      if (gtid < n) {
-        pre_s = __ldcg(A.s + gtid);
-        pre_b = A.b[gtid];
-      }
-      if (warp < 3) {
-        const double u = warp_fold_strided(A.part + warp, P, 4);
-        if (lane == 0) bc[warp] = u;
-      } else if (warp == 3) {  // sum s^2: stripe partials in stripe order
-        const double u = warp_fold_strided(A.sspart, A.stripes, 1);
-        if (lane == 0) bc[3] = u;
-      }
-    }
-    if (!peer) {
-      __syncthreads();
-      if (c == 0 && threadIdx.x == 0) ctl->tile_ctr = 0;  // every CTA is past its last claim
-      const double eta_l = __ddiv_rn(bc[0], mn);
-      const double shift_l = __dsub_rn(2.0 * eta_l, theta);
-      for (long long i = gtid; i < m; i += nthr) {
-        const double ri = i == gtid ? pre_r : __ldcg(A.r + i), ai = i == gtid ? pre_a : A.a[i];
-        A.phi[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift_l), dn);
-        A.a[i] = __dsub_rn(ai, ri);
-      }
-      for (long long j = gtid; j < n; j += nthr) {
-        const double sj = j == gtid ? pre_s : __ldcg(A.s + j), bj = j == gtid ? pre_b : A.b[j];
-        A.psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift_l), dm);
-        A.b[j] = __dsub_rn(bj, sj);
-      }
-    }
-    const double eta = __ddiv_rn(bc[0], mn);
-    stamp(P + 4);
-    const double nr2 = sqrt(bc[1]), ns2 = sqrt(bc[3]);
-    const double rp = (nr2 < ns2) ? ns2 : nr2;  // std::max semantics (solver.cpp:179)
-    theta = __dsub_rn(theta, eta);
-    ++k;
-    ++it;
-    ++epoch;
-    if (prm.fused) shifted ^= 1;
-    const long long kk = k - k0;
-    bool done = false, want_cert = false;
-    int term = TERM_MAXITER;
-    if (prm.solving) {
-      if (!(rp - rp == 0.0)) {  // solver.cpp:181-185
-        done = true;
-        term = TERM_NONFINITE;
-      } else {
-        if (rp < best * (1.0 - 1e-14)) {  // solver.cpp:200-203
-          best = rp;
-          last_imp = kk;
-        }
-        const bool at_check = (kk % prm.check_every) == 0;
-        if (at_check && rp <= prm.tol_primal && prm.has_tol_gap) {
-          // tol_gap: the launch ends here; the host runs the certificate
-          // kernels, whose finisher applies converged / stalled / max_iter
-          want_cert = true;
-        } else if (at_check && rp <= prm.tol_primal) {
-          done = true;
-          term = TERM_CONVERGED;
-        } else if (kk - last_imp >= 10000) {  // solver.cpp:17, :232-235
-          done = true;
-          term = TERM_STALLED;
-        } else if (kk >= prm.max_iter) {
-          done = true;
-          term = TERM_MAXITER;
-        }
-      }
-    } else if (it >= A.iters) {
-      done = true;
-    }
-    if (done || want_cert) {
-      if (c == 0 && threadIdx.x == 0) {
-        ctl->k = k;
-        ctl->theta[k & 1] = theta;
-        ctl->eta = eta;
-        ctl->r_primal = rp;
-        ctl->best = best;
-        ctl->last_improvement = last_imp;
-        ctl->want_cert = want_cert ? 1 : 0;
-        if (prm.solving && done) {
-          ctl->done = 1;
-          ctl->termination = term;
-        }
-        ctl->fused_shifted = shifted;
-        if (peer) *A.xep = epoch - 1;  // every CTA read the base at entry
-      }
-      break;
-    }
-    if (!peer) grid_barrier(&ctl->bar_str);  // phi / psi complete before the next sweep
+    if (stream_finish_iteration<kThreads>(A, prm, L, sred, bc, &ctl->bar_str, stamp)) break;
   }
 }
 
