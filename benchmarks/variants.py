@@ -2,8 +2,8 @@
 """Compare sweep-kernel variants (selected by environment variables, read at
 Engine creation) on one config; one JSON line per variant.
 
-  python benchmarks/variants.py headline OTDR_SWEEP=default OTDR_SWEEP=tma
-  python benchmarks/variants.py cfg3 OTDR_GL_KERNEL=ring OTDR_GL_KERNEL=stage OTDR_GL_PLAN=off
+  python benchmarks/variants.py headline OTDR_STREAM_KERNEL=tma OTDR_STREAM_KERNEL=async
+  python benchmarks/variants.py cfg3 OTDR_GL_KERNEL=pipe OTDR_GL_KERNEL=twopass
 """
 from __future__ import annotations
 

@@ -266,11 +266,8 @@ struct otdr_dev {
   double *p = nullptr, *q = nullptr, *phi = nullptr, *psi = nullptr, *a = nullptr, *b = nullptr,
          *r = nullptr, *s = nullptr;
   double *rowpart = nullptr, *colpart = nullptr, *exch = nullptr, *bpart = nullptr,
-         *cpart = nullptr, *csum = nullptr, *stage = nullptr, *fpart = nullptr, *fpart2 = nullptr;
-  int num_sms = 148, fin_grid = 1;
-  // single GPU: one cooperative finalize launch instead of reduce + update
-  // (OTDR_FINALIZE=fused opts in; measured slower than reduce + update on B200)
-  bool use_fused_finalize = false;
+         *cpart = nullptr, *csum = nullptr, *stage = nullptr;
+  int num_sms = 148;
   // on-chip resident solve (plans that fit the GPU's aggregate shared memory)
   bool allow_resident = true;
   bool sharded = false;  // NCCL exchange path (row shards, or a 1-rank communicator)
@@ -319,27 +316,10 @@ struct otdr_dev {
   // geometry
   int stripes = 1, rowgroups = 1, rows_per_cta = 1;
   int gl_stripes = 1, num_segs = 0, cert_stripes = 1, num_cert_segs = 0;
-  // single-pass cluster GL sweep plan (0 = use the two-phase fallback kernel)
-  int glc_tn = 0, glc_k = 1, glc_rows = 0;
-  size_t glc_smem = 0;
-  CUtensorMap glc_mapX{}, glc_mapC{};
-  // segment-staged GL sweep: one CTA per (segment, group of glst_g stripes)
-  int glst_g = 0, glst_groups = 0;
-  size_t glst_smem = 0;
-  // TMA box-ring GL sweep: one CTA per (segment, group of glr_g stripes)
-  int glr_g = 0, glr_groups = 0, glr_nb = 0;
-  size_t glr_smem = 0;
-  CUtensorMap glr_mapX{}, glr_mapC{};
   // pipelined single-pass GL sweep: persistent CTAs over (segment, G stripes)
   int glp_G = 0, glp_nstr = 0, glp_groups = 0, glp_lmax = 0, glp_d = 0, glp_wb = 128;
   int2* d_glp_pos = nullptr;
   size_t glp_smem = 0;
-  // TMA-pipelined plain sweep (OTDR_SWEEP=tma): box 256 cols x kSweepTR rows
-  bool use_tma_sweep = false;
-  CUtensorMap sw_mapX{}, sw_mapC{};
-  static constexpr int kSweepTR = 16;
-  static constexpr int kSweepStages = 4;     // fp32: 4 x 32 KB ring
-  static constexpr int kSweepStages64 = 3;   // fp64: 3 x 64 KB ring
   int RB = 1, CB = 1;
   size_t rowpart_cap = 0, colpart_cap = 0, cpart_cap = 0;
   std::vector<Segment> segs, cert_segs;
@@ -353,27 +333,6 @@ struct otdr_dev {
   // ---------------------------------------------------------------- launches
   static constexpr int kGLThreads = 512;
 
-  template <typename T, bool EXACT, int VW>
-  void launch_gl_cluster() {
-    auto kern = otdrk::gl_cluster_kernel<T, EXACT, VW, kGLThreads>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(glc_smem)));
-    if (glc_k > 8) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(unsigned(gl_stripes * glc_k), unsigned(num_segs), 1);
-    lc.blockDim = dim3(kGLThreads, 1, 1);
-    lc.dynamicSmemBytes = glc_smem;
-    lc.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = unsigned(glc_k);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    lc.attrs = attr;
-    lc.numAttrs = 1;
-    otdrk::GLArgs<T> ga{(T*)X, (const T*)C, phi, psi, rowpart, colpart, d_seg, d_prm, d_ctl,
-                        m_loc, ld};
-    CK(cudaLaunchKernelEx(&lc, kern, ga, glc_mapX, glc_mapC, glc_k, glc_rows));
-  }
 
   // 2-D tensor map over a row-major (m_loc x ld) matrix, box TN x R.
   void encode_map(CUtensorMap* map, void* base, int tn, int rows) {
@@ -398,18 +357,9 @@ struct otdr_dev {
     if (r != CUDA_SUCCESS) throw Error{OTDR_E_CUDA, "cuTensorMapEncodeTiled failed"};
   }
 
-  // The cluster kernel covers the plain (non-fused, untracked) iteration; the
-  // even/odd and support-tracking variants use the two-phase kernel.
+  // The pipelined kernel covers the plain (non-fused, untracked) iteration;
+  // the even/odd and support-tracking variants use the two-phase kernel.
   bool gl_pipe_active(bool track) const { return glp_G > 0 && !track && !prm.fused; }
-  bool gl_ring_active(bool track) const {
-    return !gl_pipe_active(track) && glr_g > 0 && !track && !prm.fused;
-  }
-  bool gl_stage_active(bool track) const {
-    return !gl_ring_active(track) && glst_g > 0 && !track && !prm.fused;
-  }
-  bool gl_cluster_active(bool track) const {
-    return !gl_stage_active(track) && glc_tn > 0 && !track && !prm.fused;
-  }
 
   template <typename T, int D, int WB>
   void launch_gl_pipe_t() {
@@ -499,50 +449,6 @@ struct otdr_dev {
       launch_gl_pipe();
       return;
     }
-    if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only && gl_ring_active(track)) {
-      const dim3 grid{unsigned(glr_groups), unsigned(num_segs), 1u};
-      if (f64()) {
-        otdrk::GLArgs<double> ga{(double*)X, (const double*)C, phi, psi, rowpart, colpart,
-                                 d_seg, d_prm, d_ctl, m_loc, ld};
-        CK(cudaFuncSetAttribute(otdrk::gl_ring_kernel<double, true>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(glr_smem)));
-        otdrk::gl_ring_kernel<double, true><<<grid, 512, glr_smem, stream>>>(ga, glr_mapX, glr_mapC, glr_g, glr_nb);
-      } else {
-        otdrk::GLArgs<float> ga{(float*)X, (const float*)C, phi, psi, rowpart, colpart,
-                                d_seg, d_prm, d_ctl, m_loc, ld};
-        CK(cudaFuncSetAttribute(otdrk::gl_ring_kernel<float, false>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(glr_smem)));
-        otdrk::gl_ring_kernel<float, false><<<grid, 512, glr_smem, stream>>>(ga, glr_mapX, glr_mapC, glr_g, glr_nb);
-      }
-      return;
-    }
-    if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only && gl_stage_active(track)) {
-      const dim3 grid{unsigned(glst_groups), unsigned(num_segs), 1u};
-      if (f64()) {
-        otdrk::GLArgs<double> ga{(double*)X, (const double*)C, phi, psi, rowpart, colpart,
-                                 d_seg, d_prm, d_ctl, m_loc, ld};
-        CK(cudaFuncSetAttribute(otdrk::gl_stage_kernel<double, true>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(glst_smem)));
-        otdrk::gl_stage_kernel<double, true><<<grid, 512, glst_smem, stream>>>(ga, glst_g);
-      } else {
-        otdrk::GLArgs<float> ga{(float*)X, (const float*)C, phi, psi, rowpart, colpart,
-                                d_seg, d_prm, d_ctl, m_loc, ld};
-        CK(cudaFuncSetAttribute(otdrk::gl_stage_kernel<float, false>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(glst_smem)));
-        otdrk::gl_stage_kernel<float, false><<<grid, 512, glst_smem, stream>>>(ga, glst_g);
-      }
-      return;
-    }
-    if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only && gl_cluster_active(track)) {
-      if (f64()) {
-        if (glc_tn == 64) launch_gl_cluster<double, true, 2>();
-        else launch_gl_cluster<double, true, 1>();
-      } else {
-        if (glc_tn == 128) launch_gl_cluster<float, false, 4>();
-        else launch_gl_cluster<float, false, 2>();
-      }
-      return;
-    }
     if (reg_kind == OTDR_REG_GROUP_LASSO && !sums_only) {
       dim3 grid((unsigned)((ld + tn_seg() - 1) / tn_seg()), num_segs);
       if (f64()) {
@@ -560,36 +466,6 @@ struct otdr_dev {
     }
     dim3 grid(stripes, rowgroups);
     const int so = sums_only ? 1 : 0;
-    if (use_tma_sweep && !sums_only && !track && !prm.fused) {
-      const int S = f64() ? kSweepStages64 : kSweepStages;
-      const size_t smem = 2 * size_t(S) * kSweepTR * 256 * esz + 8 * size_t(S);
-      if (f64()) {
-        otdrk::SweepArgs<double> sa{(double*)X, (const double*)C, phi, psi, rowpart, colpart,
-                                    d_prm, d_ctl, m_loc, ld, rows_per_cta, 0};
-        if (reg_kind == OTDR_REG_QUAD) {
-          auto kern = otdrk::sweep_tma_kernel<double, otdrk::REG_QUAD, true, kSweepStages64, kSweepTR>;
-          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-          kern<<<grid, otdrk::kThreads, smem, stream>>>(sa, sw_mapX, sw_mapC);
-        } else {
-          auto kern = otdrk::sweep_tma_kernel<double, otdrk::REG_NONE, true, kSweepStages64, kSweepTR>;
-          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-          kern<<<grid, otdrk::kThreads, smem, stream>>>(sa, sw_mapX, sw_mapC);
-        }
-      } else {
-        otdrk::SweepArgs<float> sa{(float*)X, (const float*)C, phi, psi, rowpart, colpart,
-                                   d_prm, d_ctl, m_loc, ld, rows_per_cta, 0};
-        if (reg_kind == OTDR_REG_QUAD) {
-          auto kern = otdrk::sweep_tma_kernel<float, otdrk::REG_QUAD, false, kSweepStages, kSweepTR>;
-          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-          kern<<<grid, otdrk::kThreads, smem, stream>>>(sa, sw_mapX, sw_mapC);
-        } else {
-          auto kern = otdrk::sweep_tma_kernel<float, otdrk::REG_NONE, false, kSweepStages, kSweepTR>;
-          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-          kern<<<grid, otdrk::kThreads, smem, stream>>>(sa, sw_mapX, sw_mapC);
-        }
-      }
-      return;
-    }
     if (f64()) {
       otdrk::SweepArgs<double> sa{(double*)X, (const double*)C, phi, psi, rowpart, colpart,
                                   d_prm, d_ctl, m_loc, ld, rows_per_cta, so};
@@ -620,9 +496,6 @@ struct otdr_dev {
   std::pair<int, int> partial_shape(bool sums_only, bool track) const {
     if (gl_active(sums_only)) {
       if (gl_pipe_active(track)) return {glp_groups, num_segs};
-      if (gl_ring_active(track)) return {glr_groups, num_segs};
-      if (gl_stage_active(track)) return {glst_groups, num_segs};
-      if (gl_cluster_active(track)) return {gl_stripes, num_segs * glc_k};
       return {int((ld + tn_seg() - 1) / tn_seg()), num_segs};
     }
     return {stripes, rowgroups};
@@ -710,21 +583,12 @@ struct otdr_dev {
     touch(otdrk::gl_stream_kernel<double, true, 2, 128>);
     touch(otdrk::gl_stream_kernel<double, true, 3, 128>);
     touch(otdrk::gl_stream_kernel<double, true, 4, 128>);
-    touch(otdrk::gl_ring_kernel<float, false>);
-    touch(otdrk::gl_ring_kernel<double, true>);
-    touch(otdrk::gl_stage_kernel<float, false>);
-    touch(otdrk::gl_stage_kernel<double, true>);
     touch(otdrk::gl_sweep_kernel<double, true, false, 1>);
     touch(otdrk::gl_sweep_kernel<double, true, true, 1>);
     touch(otdrk::gl_sweep_kernel<float, false, false, 1>);
     touch(otdrk::gl_sweep_kernel<float, false, true, 1>);
-    touch(otdrk::gl_cluster_kernel<float, false, 4, kGLThreads>);
-    touch(otdrk::gl_cluster_kernel<float, false, 2, kGLThreads>);
-    touch(otdrk::gl_cluster_kernel<double, true, 2, kGLThreads>);
-    touch(otdrk::gl_cluster_kernel<double, true, 1, kGLThreads>);
     touch(otdrk::reduce_kernel);
     touch(otdrk::update_kernel);
-    touch(otdrk::finalize_kernel);
     touch(otdrk::seed_state_kernel);
     touch(otdrk::stamp_t0_kernel);
     touch(otdrk::cert_partial_kernel<double, 1>);
@@ -779,36 +643,14 @@ struct otdr_dev {
     otdrk::cert_final_kernel<<<1, otdrk::kThreads, 0, stream>>>(fa);
   }
 
-  // Single GPU: reduce + update fused into one cooperative launch.
-  void launch_finalize(bool track, cudaGraphConditionalHandle cond, int use_cond, int cert_follows) {
-    const auto [nstripes, ngroups] = partial_shape(false, track);
-    otdrk::FinalizeArgs fa{rowpart, colpart, p, q, r, s, phi, psi, a, b, exch, fpart, fpart2,
-                           d_prm, d_ctl, m_loc, n, ld, nstripes, ngroups, cond, use_cond,
-                           cert_follows};
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(unsigned(fin_grid), 1, 1);
-    lc.blockDim = dim3(otdrk::kThreads, 1, 1);
-    lc.dynamicSmemBytes = 0;
-    lc.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    lc.attrs = attr;
-    lc.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&lc, otdrk::finalize_kernel, fa));
-  }
 
-  // One DR iteration: sweep, then (single GPU) the fused finalize, or (row
-  // shards) reduce, all-reduce of the exchange vector, update; [certificate].
+  // One DR iteration on the graph path: sweep, reduce, (row shards) all-reduce
+  // of the exchange vector, update; [certificate].
   void launch_iteration(bool track, bool cert, cudaGraphConditionalHandle cond, int use_cond) {
     launch_sweep(track, false);
-    if (!sharded && use_fused_finalize) {
-      launch_finalize(track, cond, use_cond, cert ? 1 : 0);
-    } else {
-      launch_reduce(false, track);
-      launch_exchange(exch, size_t(n) + 3);
-      launch_update(cond, use_cond, cert ? 1 : 0);
-    }
+    launch_reduce(false, track);
+    launch_exchange(exch, size_t(n) + 3);
+    launch_update(cond, use_cond, cert ? 1 : 0);
     if (cert) launch_cert(0, cond, use_cond);
   }
 
@@ -861,13 +703,9 @@ struct otdr_dev {
     if (cert_segs.empty()) cert_segs.push_back(Segment{0, 0, 0, 0});
     num_segs = int(segs.size());
     num_cert_segs = int(cert_segs.size());
-    plan_gl_cluster();
+    plan_gl();
     plan_resident();
     plan_stream();
-    if (use_tma_sweep && m_loc > 0) {
-      encode_map(&sw_mapX, X, 256, kSweepTR);
-      encode_map(&sw_mapC, C, 256, kSweepTR);
-    }
     if (d_seg) cudaFree(d_seg);
     if (d_cert_seg) cudaFree(d_cert_seg);
     d_seg = dalloc<Segment>(segs.size());
@@ -1155,19 +993,11 @@ struct otdr_dev {
   // TMA tile plan: column stripes of 256 B (else 512 B) per box row, R <= 256
   // rows per CTA (TMA box limit), a cluster of K <= 8 CTAs per class
   // segment, <= ~72 KB of tiles per CTA so three CTAs share an SM.
-  void plan_gl_cluster() {
-    glc_tn = 0;
-    glc_k = 1;
-    glc_rows = 0;
-    glc_smem = 0;
+  // Group-lasso sweep plan: the pipelined single-pass kernel when a class
+  // segment's staging fits shared memory (OTDR_GL_KERNEL=twopass forces the
+  // two-phase gl_sweep_kernel, which also serves fused / traced iterations).
+  void plan_gl() {
     gl_stripes = int((ld + tn_seg() - 1) / tn_seg());
-    glst_g = 0;
-    glst_groups = 0;
-    glst_smem = 0;
-    glr_g = 0;
-    glr_groups = 0;
-    glr_nb = 0;
-    glr_smem = 0;
     glp_G = 0;
     glp_groups = 0;
     glp_smem = 0;
@@ -1238,70 +1068,13 @@ struct otdr_dev {
         }
       }
     }
-    // segment-staged kernel: the whole segment's v for a 64-byte stripe in
-    // shared memory (<= 100 KB: two or three CTAs per SM); OTDR_GL_KERNEL
-    // selects stage / cluster / twopass explicitly.
-    const char* gk = std::getenv("OTDR_GL_KERNEL");
-    const bool want_ring = !gk || std::strcmp(gk, "ring") == 0;
-    const bool want_stage = !gk || std::strcmp(gk, "stage") == 0;
-    if (want_ring && lmax <= 1024) {
-      const long long tn = 64 / (long long)esz;
-      const long long nstr = (ld + tn - 1) / tn;
-      glr_nb = int((lmax + 255) / 256);
-      const long long work = nstr * (long long)num_segs;
-      glr_g = int(std::max<long long>(1, (work + 4LL * num_sms - 1) / (4LL * num_sms)));
-      glr_groups = int((nstr + glr_g - 1) / glr_g);
-      glr_smem = 2 * size_t(glr_nb) * 256 * 64 + size_t(glr_nb) * 256 * 8 + 2 * size_t(glr_nb) * 8;
-      encode_map(&glr_mapX, X, int(tn), 256);
-      encode_map(&glr_mapC, C, int(tn), 256);
-    }
-    const size_t stage_bytes = size_t(lmax) * (64 + 8);
-    if (want_stage && stage_bytes <= size_t(100) * 1024) {
-      const long long tn = 64 / (long long)esz;
-      const long long nstr = (ld + tn - 1) / tn;
-      glst_g = 4;  // stripes per CTA: row partials per (row, 4 stripes)
-      glst_groups = int((nstr + glst_g - 1) / glst_g);
-      glst_smem = stage_bytes;
-    }
-    if (gk && std::strcmp(gk, "twopass") == 0) return;
-    size_t tile_budget = 72 * 1024;
-    int kmin = 1;
-    int force_row_bytes = 0;
-    // Tuning hook: OTDR_GL_PLAN="tile_kb,kmin,row_bytes" or "off" (two-phase kernel).
-    if (const char* ev = std::getenv("OTDR_GL_PLAN")) {
-      if (std::strcmp(ev, "off") == 0) return;
-      int kb = 72;
-      std::sscanf(ev, "%d,%d,%d", &kb, &kmin, &force_row_bytes);
-      tile_budget = size_t(kb) * 1024;
-    }
-    for (int row_bytes : {256, 512}) {  // 256-B rows with K <= 8 measured fastest
-      if (force_row_bytes && row_bytes != force_row_bytes) continue;
-      const int tn = int(row_bytes / esz);
-      const long long rows_max =
-          std::min<long long>(256, (long long)(tile_budget / (2 * size_t(row_bytes))));
-      int k = std::max(1, kmin);
-      while (k < 8 && (lmax + k - 1) / k > rows_max) k *= 2;
-      const long long rows = (lmax + k - 1) / k;
-      if (rows > rows_max) continue;
-      glc_tn = tn;
-      glc_k = k;
-      glc_rows = int(rows);
-      const size_t creg = std::max(size_t(rows) * size_t(row_bytes),
-                                   size_t(kGLThreads / 32) * size_t(tn) * 8);
-      glc_smem = size_t(rows) * size_t(row_bytes) + creg + size_t(k + 1) * size_t(tn) * 8 +
-                 size_t(rows) * 8 + 16;
-      gl_stripes = int((ld + tn - 1) / tn);
-      encode_map(&glc_mapX, X, tn, glc_rows);
-      encode_map(&glc_mapC, C, tn, glc_rows);
-      return;
-    }
   }
 
   void ensure_partials() {
     const int seg_stripes = int((ld + tn_seg() - 1) / tn_seg());
-    const size_t need_row = size_t(std::max(std::max(std::max(stripes, gl_stripes), std::max(seg_stripes, glst_groups)), std::max(glr_groups, glp_groups))) *
+    const size_t need_row = size_t(std::max(std::max(stripes, gl_stripes), std::max(seg_stripes, glp_groups))) *
                             size_t(std::max<long long>(m_loc, 1));
-    const size_t need_col = size_t(std::max(rowgroups, num_segs * std::max(glc_k, 1))) * size_t(ld);
+    const size_t need_col = size_t(std::max(rowgroups, num_segs)) * size_t(ld);
     const size_t need_c = size_t(cert_stripes) * size_t(num_cert_segs) * otdrk::kCertVals;
     if (need_row > rowpart_cap) {
       if (rowpart) cudaFree(rowpart);
@@ -1564,7 +1337,7 @@ struct otdr_dev {
     }
     void* ptrs[] = {C, X, p, q, phi, psi, a, b, r, s, rowpart, colpart, exch, bpart, cpart,
                     str_part, str_colpart, d_sfirst, d_scnt, str_sspart, d_glp_pos,
-                    csum, stage, fpart, fpart2, gscratch, d_dev_row, d_seg, d_cert_seg, d_prm, d_ctl, d_trace, d_mx};
+                    csum, stage, gscratch, d_dev_row, d_seg, d_cert_seg, d_prm, d_ctl, d_trace, d_mx};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);
     if (h_ctl) cudaFreeHost(h_ctl);
@@ -1694,8 +1467,8 @@ otdr_status otdr_dev_peer_link_local(otdr_dev** ctxs, int nranks) {
 
 int otdr_dev_kernels_per_iteration(const otdr_dev* ctx) {
   if (otdr_dev_solve_path(ctx) != OTDR_PATH_GRAPH) return 0;
-  // sweep + finalize (single GPU) / sweep + reduce + update
-  return (ctx && (ctx->comm || !ctx->use_fused_finalize)) ? 3 : 2;
+  // sweep + reduce + update (+ the NCCL all-reduce when row-sharded)
+  return 3;
 }
 
 otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
@@ -1784,9 +1557,7 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     CK(cudaMemset(ctx->s, 0, size_t(ctx->ld) * 8));
     ctx->exch = dalloc<double>(size_t(ctx->n) + 3);
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
-    if (const char* fe = std::getenv("OTDR_FINALIZE")) ctx->use_fused_finalize = std::strcmp(fe, "fused") == 0;
     if (const char* re = std::getenv("OTDR_RESIDENT")) ctx->allow_resident = std::strcmp(re, "off") != 0;
-    if (const char* se = std::getenv("OTDR_SWEEP")) ctx->use_tma_sweep = std::strcmp(se, "tma") == 0;
     if (const char* st = std::getenv("OTDR_STREAM")) ctx->allow_stream = std::strcmp(st, "off") != 0;
     if (const char* gs = std::getenv("OTDR_GL_STREAM")) ctx->allow_gl_stream = std::strcmp(gs, "off") != 0;
     ctx->str_d = -1;
@@ -1795,18 +1566,6 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     if (const char* sd = std::getenv("OTDR_STREAM_D")) ctx->str_d = std::atoi(sd);
     if (const char* sk = std::getenv("OTDR_STREAM_KERNEL")) ctx->str_kind = std::strcmp(sk, "async") == 0 ? 0 : 1;
     if (const char* tc = std::getenv("OTDR_TS_CFG")) ctx->ts_cfg = std::atoi(tc);
-    {
-      int occ = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, otdrk::finalize_kernel,
-                                                       otdrk::kThreads, 0));
-      // enough warps for one warp per row in a single pass (rows read their
-      // stripe partials warp-wide), capped at full co-residency
-      const long long want = std::max<long long>(
-          1, (std::max(ctx->m_loc, ctx->n) + otdrk::kWarps - 1) / otdrk::kWarps);
-      ctx->fin_grid = int(std::min<long long>(want, (long long)ctx->num_sms * std::max(occ, 1)));
-      ctx->fpart = dalloc<double>(size_t(ctx->fin_grid) * 3);
-      ctx->fpart2 = dalloc<double>(size_t(ctx->fin_grid));
-    }
     ctx->plan_geometry();
     ctx->bpart = dalloc<double>(size_t(ctx->RB + ctx->CB) * 3);
     ctx->csum = dalloc<double>(otdrk::kCertVals);
@@ -2219,17 +1978,11 @@ otdr_status otdr_dev_profile(otdr_dev* ctx, double rho, int64_t iters, otdr_kern
       CK(cudaEventRecord(ev[0], ctx->stream));
       ctx->launch_sweep(false, false);
       CK(cudaEventRecord(ev[1], ctx->stream));
-      if (ctx->comm == nullptr && ctx->use_fused_finalize) {  // reduce_ms = fused finalize
-        ctx->launch_finalize(false, 0, 0, 0);
-        CK(cudaEventRecord(ev[2], ctx->stream));
-        CK(cudaEventRecord(ev[3], ctx->stream));
-      } else {
-        ctx->launch_reduce(false, false);
-        CK(cudaEventRecord(ev[2], ctx->stream));
-        ctx->launch_exchange(ctx->exch, size_t(ctx->n) + 3);
-        CK(cudaEventRecord(ev[3], ctx->stream));
-        ctx->launch_update(0, 0, 0);
-      }
+      ctx->launch_reduce(false, false);
+      CK(cudaEventRecord(ev[2], ctx->stream));
+      ctx->launch_exchange(ctx->exch, size_t(ctx->n) + 3);
+      CK(cudaEventRecord(ev[3], ctx->stream));
+      ctx->launch_update(0, 0, 0);
       CK(cudaEventRecord(ev[4], ctx->stream));
       ctx->check_launch();
       CK(cudaEventSynchronize(ev[4]));

@@ -533,171 +533,7 @@ __global__ void __launch_bounds__(kThreads) gl_sweep_kernel(GLArgs<T> a) {
   }
 }
 
-// ----------------------------- group-lasso sweep, single pass (segment-staged)
-// One CTA owns a whole class segment for a narrow stripe of TN columns
-// (TN*sizeof(T) = 64 bytes: four lanes cover one row with 16-byte vectors, a
-// warp covers 8 rows per instruction). Phase 1 streams the segment's C and X
-// rows once, keeps v = [((X - rho C) + phi) + psi]_+ in shared memory and
-// accumulates the per-column ||v_g||^2; after one __syncthreads the block
-// soft-threshold scale of every column is known and phase 2 writes
-// X = v * scale from shared memory. No cluster and no re-read: 12 B per entry
-// (fp32), the segment tile (L x 64 B) limits L to the shared-memory budget.
-template <typename T, bool EXACT>
-__global__ void __launch_bounds__(512, 2) gl_stage_kernel(GLArgs<T> a, int G) {
-  using V = typename Vec<T>::type;
-  constexpr int VEC = Vec<T>::N;      // 4 floats / 2 doubles per lane
-  constexpr int TN = 64 / sizeof(T);  // 16 floats / 8 doubles: 64 B per row
-  constexpr int LPR = TN / VEC;       // lanes per row (4)
-  constexpr int RPW = 32 / LPR;       // rows per warp instruction (8)
-  constexpr int NW = 16;
-  constexpr int U = 2;                // row passes in flight
-  constexpr int ROWS_PER_PASS = NW * RPW;  // 128
-  const Ctl* ctl = a.ctl;
-  if (ctl->done) return;
-  const Segment sg = a.seg[blockIdx.y];
-  const int L = (int)(sg.end - sg.begin);
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* vt = reinterpret_cast<T*>(smem_raw);                                  // L x TN staged v
-  double* rowacc = reinterpret_cast<double*>(smem_raw + (size_t)L * TN * sizeof(T));  // L
-  __shared__ double red[NW][TN];
-  __shared__ double sig[TN];
-
-  const Params& prm = *a.prm;
-  const double rho = prm.rho, thr = prm.gl_thr;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int sub = lane % LPR, rsub = lane / LPR;
-  const long long group = blockIdx.x;  // this CTA sweeps stripes group*G .. group*G+G-1
-  const int ngroups = gridDim.x;
-  for (int t = threadIdx.x; t < L; t += 512) rowacc[t] = 0.0;
-
-  for (int gs = 0; gs < G; ++gs) {
-    const long long stripe = group * G + gs;
-    const long long col0 = stripe * TN + sub * VEC;
-    if (stripe * TN >= a.ld) break;  // CTA-uniform
-    const bool cok = col0 < a.ld;
-    double psi_r[VEC], sq[VEC], cacc[VEC];
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      psi_r[e] = cok ? a.psi[col0 + e] : 0.0;
-      sq[e] = 0.0;
-      cacc[e] = 0.0;
-    }
-    // phase 1: v -> smem, per-column sum of v^2
-    for (int p0 = 0; p0 < L; p0 += ROWS_PER_PASS * U) {
-      V xv[U], cv[U];
-      double ph[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int t = p0 + u * ROWS_PER_PASS + warp * RPW + rsub;
-        if (cok && t < L) {
-          const long long i = sg.begin + t;
-          ph[u] = a.phi[i];
-          xv[u] = ld_rw(reinterpret_cast<const V*>(a.X + i * a.ld + col0));
-          cv[u] = ld_ro(reinterpret_cast<const V*>(a.C + i * a.ld + col0));
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int t = p0 + u * ROWS_PER_PASS + warp * RPW + rsub;
-        if (cok && t < L) {
-          double x[VEC], c[VEC], o[VEC];
-          unpack(xv[u], x);
-          unpack(cv[u], c);
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, c[e])), ph[u]), psi_r[e])
-                                     : (fma(-rho, c[e], x[e]) + ph[u]) + psi_r[e];
-            const double v = clamp0(val);
-            o[e] = v;
-            sq[e] += v * v;
-          }
-          reinterpret_cast<V*>(vt + (size_t)t * TN)[sub] = pack<T>(o);
-        }
-      }
-    }
-    // per-column norms: lanes sharing `sub` (xor 4, 8, 16), then warps
-#pragma unroll
-    for (int e = 0; e < VEC; ++e)
-#pragma unroll
-      for (int o = LPR; o < 32; o <<= 1) sq[e] += __shfl_xor_sync(0xffffffffu, sq[e], o);
-    if (rsub == 0) {
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) red[warp][sub * VEC + e] = sq[e];
-    }
-    __syncthreads();
-    if (threadIdx.x < TN) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) s += red[w][threadIdx.x];
-      const double nrm = sqrt(s);
-      sig[threadIdx.x] = !sg.grouped ? 1.0
-                         : (nrm <= thr) ? 0.0
-                                        : (EXACT ? __dsub_rn(1.0, __ddiv_rn(thr, nrm)) : 1.0 - thr / nrm);
-    }
-    __syncthreads();
-    double sc[VEC];
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) sc[e] = sig[sub * VEC + e];
-    // phase 2: X = v * scale from smem; row sums into rowacc; column sums
-    for (int t0 = 0; t0 < L; t0 += ROWS_PER_PASS) {
-      const int t = t0 + warp * RPW + rsub;
-      double rs = 0.0;
-      if (cok && t < L) {
-        const long long i = sg.begin + t;
-        double v[VEC], o[VEC];
-        unpack(reinterpret_cast<const V*>(vt + (size_t)t * TN)[sub], v);
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const double nx = sg.grouped ? (EXACT ? __dmul_rn(v[e], sc[e]) : v[e] * sc[e]) : v[e];
-          o[e] = nx;
-          cacc[e] += nx;
-          rs += nx;
-        }
-        reinterpret_cast<V*>(a.X + i * a.ld)[col0 / VEC] = pack<T>(o);
-      }
-#pragma unroll
-      for (int o = 1; o < LPR; o <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
-      if (sub == 0 && t < L) rowacc[t] += rs;  // one (warp, rsub) per row: no race
-    }
-#pragma unroll
-    for (int e = 0; e < VEC; ++e)
-#pragma unroll
-      for (int o = LPR; o < 32; o <<= 1) cacc[e] += __shfl_xor_sync(0xffffffffu, cacc[e], o);
-    __syncthreads();  // red reused; v tile reused by the next stripe
-    if (rsub == 0) {
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) red[warp][sub * VEC + e] = cacc[e];
-    }
-    __syncthreads();
-    if (threadIdx.x < TN) {
-      const long long col = stripe * TN + threadIdx.x;
-      if (col < a.ld) {
-        double s = 0.0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) s += red[w][threadIdx.x];
-        a.colpart[(long long)blockIdx.y * a.ld + col] = s;
-      }
-    }
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < L; t += 512)
-    a.rowpart[(sg.begin + t) * (long long)ngroups + group] = rowacc[t];
-}
-
-// ------------------------------------- group-lasso sweep, single pass (cluster)
-// The B200 form of the group-lasso sweep. One thread-block CLUSTER of K CTAs
-// owns a (class segment, 256-byte column stripe) tile; CTA k of the cluster
-// owns R rows of the segment. Its C and X tiles (R x TN) arrive in shared
-// memory through two 2-D TMA loads (cp.async.bulk.tensor, mbarrier
-// completion), so all of the CTA's bytes are in flight at once with no
-// register staging. Phase 1 computes v = [((X - rho C) + phi) + psi]_+ from the
-// tiles, overwrites the X tile with v and reduces per-column ||v_g||^2. The K
-// partial norms are combined through distributed shared memory (every CTA sums
-// them in the same rank order, so all agree bit-for-bit), the block
-// soft-threshold scale is formed (regularizers.cpp:85-99), and phase 2 writes
-// X = v * scale once: 12 B per entry of HBM traffic in fp32 storage.
-// Staging precision is T: fp64 storage stages fp64 v (element-wise identical
-// to the reference); fp32 storage stages fp32 v (<= 1 ulp(fp32) from v*scale).
+// ------------------------------------------------ TMA / mbarrier helpers
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -728,506 +564,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(dst)),
       "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(smem_addr(bar))
       : "memory");
-}
-
-template <typename T, bool EXACT, int VW, int NT>
-__global__ void __launch_bounds__(NT) gl_cluster_kernel(GLArgs<T> a,
-                                                       const __grid_constant__ CUtensorMap mapX,
-                                                       const __grid_constant__ CUtensorMap mapC,
-                                                       int K, int R) {
-  namespace cg = cooperative_groups;
-  constexpr int TN = 32 * VW;  // one TMA box row: 256 or 512 bytes
-  constexpr int NW = NT / 32;
-  const Ctl* ctl = a.ctl;
-  if (ctl->done) return;  // grid-uniform: every CTA of every cluster returns together
-  cg::cluster_group cluster = cg::this_cluster();
-  const int crank = (int)cluster.block_rank();
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* tileX = reinterpret_cast<T*>(smem_raw);                 // R x TN (then v)
-  T* tileC = tileX + (size_t)R * TN;                          // R x TN (then reduction scratch)
-  double* red = reinterpret_cast<double*>(tileC);             // NW x TN, after phase 1
-  const size_t creg = max((size_t)R * TN * sizeof(T), (size_t)NW * TN * sizeof(double));
-  double* psq = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(tileC) + creg);  // K x TN
-  double* sig = psq + (size_t)K * TN;                         // TN
-  double* phs = sig + TN;                                     // R (phi of own rows)
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(phs + R);
-
-  const Params& prm = *a.prm;
-  const double rho = prm.rho, thr = prm.gl_thr;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nstripes = gridDim.x / K;
-  const long long stripe = blockIdx.x / K;
-  const long long colbase = stripe * TN;
-  const long long col0 = colbase + lane * VW;
-  const bool cok = col0 < a.ld;
-  const Segment sg = a.seg[blockIdx.y];
-  const long long r0 = sg.begin + (long long)crank * R;
-  long long r1 = r0 + R;
-  if (r1 > sg.end) r1 = sg.end;
-  const int nrows = r1 > r0 ? (int)(r1 - r0) : 0;
-
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    if (nrows > 0) {
-      // full boxes (rows past the segment / matrix and columns past ld are
-      // loaded or zero-filled, never used)
-      mbar_expect_tx(bar, 2u * (unsigned)(R * TN * sizeof(T)));
-      tma_load_2d(tileX, &mapX, (int)colbase, (int)r0, bar);
-      tma_load_2d(tileC, &mapC, (int)colbase, (int)r0, bar);
-    }
-  }
-  for (int t = threadIdx.x; t < nrows; t += NT) phs[t] = a.phi[r0 + t];
-  // split cluster barrier: arrive now, wait before the first DSMEM store, so
-  // every peer CTA has started before its shared memory is written
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-  double psi_r[VW], sq[VW], cacc[VW];
-#pragma unroll
-  for (int e = 0; e < VW; ++e) {
-    psi_r[e] = cok ? a.psi[col0 + e] : 0.0;
-    sq[e] = 0.0;
-    cacc[e] = 0.0;
-  }
-  __syncthreads();  // barrier initialised and phi staged
-  if (nrows > 0) mbar_wait(bar, 0);
-
-  // phase 1 (from shared memory): v -> X tile, per-column sum of v^2
-  if (cok) {
-    for (int t = warp; t < nrows; t += NW) {
-      const double ph = phs[t];
-      T* xr = tileX + (size_t)t * TN + lane * VW;
-      const T* cr = tileC + (size_t)t * TN + lane * VW;
-      double x[VW], c[VW], o[VW];
-      if constexpr (VW * sizeof(T) == 16) {
-        unpack(*reinterpret_cast<const typename Vec<T>::type*>(xr), x);
-        unpack(*reinterpret_cast<const typename Vec<T>::type*>(cr), c);
-      } else {
-#pragma unroll
-        for (int e = 0; e < VW; ++e) {
-          x[e] = (double)xr[e];
-          c[e] = (double)cr[e];
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < VW; ++e) {
-        const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, c[e])), ph), psi_r[e])
-                                 : (fma(-rho, c[e], x[e]) + ph) + psi_r[e];
-        const double v = clamp0(val);
-        o[e] = v;
-        sq[e] += v * v;
-      }
-      if constexpr (VW * sizeof(T) == 16) {
-        *reinterpret_cast<typename Vec<T>::type*>(xr) = pack<T>(o);
-      } else {
-#pragma unroll
-        for (int e = 0; e < VW; ++e) xr[e] = (T)o[e];
-      }
-    }
-  }
-  __syncthreads();  // C tile no longer needed: reuse as reduction scratch
-  if (sg.grouped) {
-#pragma unroll
-    for (int e = 0; e < VW; ++e) red[warp * TN + lane * VW + e] = sq[e];
-  }
-  __syncthreads();
-  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-  if (sg.grouped) {
-    // push this CTA's per-column partial norms into slot [crank] of every
-    // peer's table (DSMEM stores), so that after ONE cluster barrier each CTA
-    // reads only its own shared memory
-    for (int t = threadIdx.x; t < TN * K; t += NT) {
-      const int col = t % TN, k = t / TN;
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) s += red[w * TN + col];
-      *cluster.map_shared_rank(psq + (size_t)crank * TN + col, k) = s;
-    }
-  }
-  cluster.sync();  // every CTA's partial norms are in every CTA's table
-  if (sg.grouped) {
-    for (int t = threadIdx.x; t < TN; t += NT) {
-      double s = 0.0;
-      for (int k = 0; k < K; ++k) s += psq[(size_t)k * TN + t];  // fixed rank order
-      const double nrm = sqrt(s);
-      sig[t] = (nrm <= thr) ? 0.0 : (EXACT ? __dsub_rn(1.0, __ddiv_rn(thr, nrm)) : 1.0 - thr / nrm);
-    }
-  } else {
-    for (int t = threadIdx.x; t < TN; t += NT) sig[t] = 1.0;
-  }
-  __syncthreads();  // the scale is visible (no DSMEM traffic after the barrier)
-  double sc[VW];
-#pragma unroll
-  for (int e = 0; e < VW; ++e) sc[e] = sig[lane * VW + e];
-
-  // phase 2: X = v * scale, row partials (8-row reduce-scatter), column partials
-  for (int t0 = warp * 8; t0 < nrows; t0 += NW * 8) {
-    double rs[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int t = t0 + u;
-      rs[u] = 0.0;
-      if (cok && t < nrows) {
-        const long long i = r0 + t;
-        const T* vr = tileX + (size_t)t * TN + lane * VW;
-        double v[VW], o[VW];
-        if constexpr (VW * sizeof(T) == 16) {
-          unpack(*reinterpret_cast<const typename Vec<T>::type*>(vr), v);
-        } else {
-#pragma unroll
-          for (int e = 0; e < VW; ++e) v[e] = (double)vr[e];
-        }
-#pragma unroll
-        for (int e = 0; e < VW; ++e) {
-          const double nx = sg.grouped ? (EXACT ? __dmul_rn(v[e], sc[e]) : v[e] * sc[e]) : v[e];
-          o[e] = nx;
-          cacc[e] += nx;
-          rs[u] += nx;
-        }
-        if constexpr (VW * sizeof(T) == 16) {
-          *reinterpret_cast<typename Vec<T>::type*>(a.X + i * a.ld + col0) = pack<T>(o);
-        } else if constexpr (VW == 2 && sizeof(T) == 4) {
-          *reinterpret_cast<float2*>(a.X + i * a.ld + col0) =
-              make_float2(__double2float_rn(o[0]), __double2float_rn(o[1]));
-        } else {
-#pragma unroll
-          for (int e = 0; e < VW; ++e) a.X[i * a.ld + col0 + e] = (T)o[e];
-        }
-      }
-    }
-    const double tot = reduce8_rows(rs, lane);
-    const int t = t0 + row8_of(lane);
-    if ((lane & 3) == 0 && t < nrows) a.rowpart[(r0 + t) * (long long)nstripes + stripe] = tot;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int e = 0; e < VW; ++e) red[warp * TN + lane * VW + e] = cacc[e];
-  __syncthreads();
-  for (int t = threadIdx.x; t < TN; t += NT) {
-    const long long col = colbase + t;
-    if (col < a.ld) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) s += red[w * TN + t];
-      a.colpart[((long long)blockIdx.y * K + crank) * a.ld + col] = s;
-    }
-  }
-}
-
-// --------------------------------------------------- TMA-pipelined sweep
-// The plain iteration (zero / quadratic, not fused, untracked) with C and X
-// tiles staged by 2-D TMA through an S-stage shared-memory ring: the CTA keeps
-// S-1 tiles (TR rows x 256 columns of C and X) in flight while it computes
-// the oldest one, so HBM sees a steady stream independent of register
-// pressure. Same partial-sum layout as sweep_kernel (rowpart[row][stripe],
-// colpart[rowgroup][col]) and the same element-wise arithmetic.
-template <typename T, int REG, bool EXACT, int S, int TR>
-__global__ void __launch_bounds__(kThreads, 1) sweep_tma_kernel(SweepArgs<T> a,
-                                                                const __grid_constant__ CUtensorMap mapX,
-                                                                const __grid_constant__ CUtensorMap mapC) {
-  using V = typename Vec<T>::type;
-  constexpr int VEC = Vec<T>::N;
-  constexpr int TN = 256;
-  constexpr int NV = TN / (32 * VEC);
-  constexpr unsigned kTileBytes = (unsigned)(TR * TN * sizeof(T));
-  const Ctl* ctl = a.ctl;
-  if (ctl->done) return;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* ring = reinterpret_cast<T*>(smem_raw);  // S x {X tile, C tile}
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + 2 * S * kTileBytes);
-  __shared__ double red[kWarps][TN];
-
-  const Params& prm = *a.prm;
-  const double rho = prm.rho, qd = prm.quad_d, qinv = prm.quad_inv;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long stripe = blockIdx.x;
-  const long long col0 = stripe * TN;
-  const long long r_begin = (long long)blockIdx.y * a.rows_per_cta;
-  long long r_end = r_begin + a.rows_per_cta;
-  if (r_end > a.m) r_end = a.m;
-  const int ntiles = r_end > r_begin ? (int)((r_end - r_begin + TR - 1) / TR) : 0;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
-    for (int s = 0; s < S && s < ntiles; ++s) {
-      T* xt = ring + (size_t)s * 2 * TR * TN;
-      mbar_expect_tx(&full[s], 2 * kTileBytes);
-      tma_load_2d(xt, &mapX, (int)col0, (int)(r_begin + (long long)s * TR), &full[s]);
-      tma_load_2d(xt + TR * TN, &mapC, (int)col0, (int)(r_begin + (long long)s * TR), &full[s]);
-    }
-  }
-  long long cols[NV];
-  bool cok[NV];
-  double psi_r[NV][VEC], cacc[NV][VEC];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    cols[v] = col0 + v * 32 * VEC + lane * VEC;
-    cok[v] = cols[v] < a.ld;
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      psi_r[v][e] = cok[v] ? a.psi[cols[v] + e] : 0.0;
-      cacc[v][e] = 0.0;
-    }
-  }
-  __syncthreads();
-
-  for (int it = 0; it < ntiles; ++it) {
-    const int s = it % S;
-    mbar_wait(&full[s], (unsigned)((it / S) & 1));
-    const T* xt = ring + (size_t)s * 2 * TR * TN;
-    const T* ct = xt + TR * TN;
-    const long long row0 = r_begin + (long long)it * TR;
-    // TR/kWarps rows per warp, their shuffle chains interleaved
-    constexpr int RPW = TR / kWarps;
-    double rs[RPW];
-#pragma unroll
-    for (int u = 0; u < RPW; ++u) {
-      const int t = warp + u * kWarps;
-      const long long i = row0 + t;
-      rs[u] = 0.0;
-      if (i < r_end) {
-        const double ph = a.phi[i];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          if (!cok[v]) continue;
-          double x[VEC], c[VEC], o[VEC];
-          unpack(reinterpret_cast<const V*>(xt + (size_t)t * TN)[v * 32 + lane], x);
-          unpack(reinterpret_cast<const V*>(ct + (size_t)t * TN)[v * 32 + lane], c);
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, c[e])), ph), psi_r[v][e])
-                                     : (fma(-rho, c[e], x[e]) + ph) + psi_r[v][e];
-            double nx = clamp0(val);
-            if (REG == REG_QUAD) nx = EXACT ? div_rn_by(nx, qd, qinv) : nx * qinv;
-            o[e] = nx;
-            cacc[v][e] += nx;
-            rs[u] += nx;
-          }
-          reinterpret_cast<V*>(a.X + i * a.ld)[cols[v] / VEC] = pack<T>(o);
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int u = 0; u < RPW; ++u) rs[u] += __shfl_xor_sync(0xffffffffu, rs[u], o);
-    if (lane == 0) {
-#pragma unroll
-      for (int u = 0; u < RPW; ++u) {
-        const long long i = row0 + warp + u * kWarps;
-        if (i < r_end) a.rowpart[i * (long long)gridDim.x + stripe] = rs[u];
-      }
-    }
-    __syncthreads();  // stage s fully consumed
-    if (threadIdx.x == 0 && it + S < ntiles) {
-      T* dst = ring + (size_t)s * 2 * TR * TN;
-      mbar_expect_tx(&full[s], 2 * kTileBytes);
-      tma_load_2d(dst, &mapX, (int)col0, (int)(r_begin + (long long)(it + S) * TR), &full[s]);
-      tma_load_2d(dst + TR * TN, &mapC, (int)col0, (int)(r_begin + (long long)(it + S) * TR), &full[s]);
-    }
-  }
-#pragma unroll
-  for (int v = 0; v < NV; ++v)
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) red[warp][v * 32 * VEC + lane * VEC + e] = cacc[v][e];
-  __syncthreads();
-  for (int t = threadIdx.x; t < TN; t += kThreads) {
-    const long long col = col0 + t;
-    if (col < a.ld) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) s += red[w][t];
-      a.colpart[(long long)blockIdx.y * a.ld + col] = s;
-    }
-  }
-}
-
-// ------------------------------ group-lasso sweep, single pass (TMA box ring)
-// Segment-staged like gl_stage_kernel, but C and X arrive as 2-D TMA boxes
-// (64 B x 256 rows) into per-box shared-memory buffers with mbarrier
-// completion, and every buffer is refilled for the NEXT stripe as soon as it
-// is consumed: a C box right after phase 1 used it, an X box (holding v) right
-// after phase 2 wrote it back. HBM therefore streams continuously while the
-// CTA alternates between the norm phase and the scaling phase.
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-template <typename T, bool EXACT>
-__global__ void __launch_bounds__(512, 1) gl_ring_kernel(GLArgs<T> a,
-                                                        const __grid_constant__ CUtensorMap mapX,
-                                                        const __grid_constant__ CUtensorMap mapC,
-                                                        int G, int NB) {
-  using V = typename Vec<T>::type;
-  constexpr int VEC = Vec<T>::N;
-  constexpr int TN = 64 / sizeof(T);
-  constexpr int LPR = TN / VEC;            // 4 lanes per row
-  constexpr int RPW = 32 / LPR;            // 8 rows per warp instruction
-  constexpr int NW = 16;
-  constexpr int BR = 256;                  // rows per TMA box
-  constexpr unsigned kBox = BR * 64;       // bytes per box
-  const Ctl* ctl = a.ctl;
-  if (ctl->done) return;
-  const Segment sg = a.seg[blockIdx.y];
-  const int L = (int)(sg.end - sg.begin);
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* xb = reinterpret_cast<T*>(smem_raw);                         // NB boxes (X, then v)
-  T* cb = reinterpret_cast<T*>(smem_raw + (size_t)NB * kBox);     // NB boxes (C)
-  double* rowacc = reinterpret_cast<double*>(smem_raw + 2 * (size_t)NB * kBox);  // NB*BR
-  unsigned long long* fx = reinterpret_cast<unsigned long long*>(rowacc + (size_t)NB * BR);
-  unsigned long long* fc = fx + NB;
-  __shared__ double red[NW][TN];
-  __shared__ double sig[TN];
-
-  const Params& prm = *a.prm;
-  const double rho = prm.rho, thr = prm.gl_thr;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int sub = lane % LPR, rsub = lane / LPR;
-  const long long group = blockIdx.x;
-  const int ngroups = gridDim.x;
-  int nstr = G;
-  {
-    const long long first = group * G;
-    const long long total = (a.ld + TN - 1) / TN;
-    if (first + nstr > total) nstr = (int)(total - first);
-  }
-  const int nbox = (L + BR - 1) / BR;
-  auto issue = [&](const CUtensorMap* map, T* buf, unsigned long long* bar, long long stripe, int kb) {
-    mbar_expect_tx(bar, kBox);
-    tma_load_2d(buf, map, (int)(stripe * TN), (int)(sg.begin + (long long)kb * BR), bar);
-  };
-  if (threadIdx.x == 0) {
-    for (int kb = 0; kb < NB; ++kb) {
-      mbar_init(&fx[kb], 1);
-      mbar_init(&fc[kb], 1);
-    }
-    if (nstr > 0)
-      for (int kb = 0; kb < nbox; ++kb) {
-        issue(&mapX, xb + (size_t)kb * BR * TN, &fx[kb], group * G, kb);
-        issue(&mapC, cb + (size_t)kb * BR * TN, &fc[kb], group * G, kb);
-      }
-  }
-  for (int t = threadIdx.x; t < nbox * BR; t += 512) rowacc[t] = 0.0;
-  __syncthreads();
-
-  for (int si = 0; si < nstr; ++si) {
-    const long long stripe = group * G + si;
-    const bool has_next = si + 1 < nstr;
-    const unsigned par = (unsigned)(si & 1);
-    const long long col0 = stripe * TN + sub * VEC;
-    const bool cok = col0 < a.ld;
-    double psi_r[VEC], sq[VEC], cacc[VEC];
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      psi_r[e] = cok ? a.psi[col0 + e] : 0.0;
-      sq[e] = 0.0;
-      cacc[e] = 0.0;
-    }
-    // phase 1, box by box
-    for (int kb = 0; kb < nbox; ++kb) {
-      mbar_wait(&fx[kb], par);
-      mbar_wait(&fc[kb], par);
-      T* xt = xb + (size_t)kb * BR * TN;
-      const T* ct = cb + (size_t)kb * BR * TN;
-#pragma unroll
-      for (int pass = 0; pass < BR / (NW * RPW); ++pass) {
-        const int r = pass * NW * RPW + warp * RPW + rsub;  // row within the box
-        const int t = kb * BR + r;                          // row within the segment
-        if (cok && t < L) {
-          const double ph = a.phi[sg.begin + t];
-          double x[VEC], c[VEC], o[VEC];
-          unpack(reinterpret_cast<const V*>(xt + (size_t)r * TN)[sub], x);
-          unpack(reinterpret_cast<const V*>(ct + (size_t)r * TN)[sub], c);
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            const double val = EXACT ? __dadd_rn(__dadd_rn(__dsub_rn(x[e], __dmul_rn(rho, c[e])), ph), psi_r[e])
-                                     : (fma(-rho, c[e], x[e]) + ph) + psi_r[e];
-            const double v = clamp0(val);
-            o[e] = v;
-            sq[e] += v * v;
-          }
-          reinterpret_cast<V*>(xt + (size_t)r * TN)[sub] = pack<T>(o);
-        }
-      }
-      __syncthreads();  // C box kb consumed by every thread
-      if (threadIdx.x == 0 && has_next) {
-        fence_proxy_async_smem();
-        issue(&mapC, cb + (size_t)kb * BR * TN, &fc[kb], stripe + 1, kb);
-      }
-    }
-    // per-column norms
-#pragma unroll
-    for (int e = 0; e < VEC; ++e)
-#pragma unroll
-      for (int o = LPR; o < 32; o <<= 1) sq[e] += __shfl_xor_sync(0xffffffffu, sq[e], o);
-    if (rsub == 0) {
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) red[warp][sub * VEC + e] = sq[e];
-    }
-    __syncthreads();
-    if (threadIdx.x < TN) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) s += red[w][threadIdx.x];
-      const double nrm = sqrt(s);
-      sig[threadIdx.x] = !sg.grouped ? 1.0
-                         : (nrm <= thr) ? 0.0
-                                        : (EXACT ? __dsub_rn(1.0, __ddiv_rn(thr, nrm)) : 1.0 - thr / nrm);
-    }
-    __syncthreads();
-    double sc[VEC];
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) sc[e] = sig[sub * VEC + e];
-    // phase 2, box by box; each X box is refilled with the next stripe once written back
-    for (int kb = 0; kb < nbox; ++kb) {
-      const T* vt = xb + (size_t)kb * BR * TN;
-#pragma unroll
-      for (int pass = 0; pass < BR / (NW * RPW); ++pass) {
-        const int r = pass * NW * RPW + warp * RPW + rsub;
-        const int t = kb * BR + r;
-        double rs = 0.0;
-        if (cok && t < L) {
-          double v[VEC], o[VEC];
-          unpack(reinterpret_cast<const V*>(vt + (size_t)r * TN)[sub], v);
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            const double nx = sg.grouped ? (EXACT ? __dmul_rn(v[e], sc[e]) : v[e] * sc[e]) : v[e];
-            o[e] = nx;
-            cacc[e] += nx;
-            rs += nx;
-          }
-          reinterpret_cast<V*>(a.X + (sg.begin + t) * a.ld)[col0 / VEC] = pack<T>(o);
-        }
-#pragma unroll
-        for (int o = 1; o < LPR; o <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
-        if (sub == 0 && t < L) rowacc[t] += rs;
-      }
-      __syncthreads();  // X box kb written back by every thread
-      if (threadIdx.x == 0 && has_next) {
-        fence_proxy_async_smem();  // generic writes of v before the async-proxy refill
-        issue(&mapX, xb + (size_t)kb * BR * TN, &fx[kb], stripe + 1, kb);
-      }
-    }
-#pragma unroll
-    for (int e = 0; e < VEC; ++e)
-#pragma unroll
-      for (int o = LPR; o < 32; o <<= 1) cacc[e] += __shfl_xor_sync(0xffffffffu, cacc[e], o);
-    if (rsub == 0) {
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) red[warp][sub * VEC + e] = cacc[e];
-    }
-    __syncthreads();
-    if (threadIdx.x < TN) {
-      const long long col = stripe * TN + threadIdx.x;
-      if (col < a.ld) {
-        double s = 0.0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) s += red[w][threadIdx.x];
-        a.colpart[(long long)blockIdx.y * a.ld + col] = s;
-      }
-    }
-    __syncthreads();  // red reused by the next stripe
-  }
-  for (int t = threadIdx.x; t < L; t += 512)
-    a.rowpart[(sg.begin + t) * (long long)ngroups + group] = rowacc[t];
 }
 
 // ---------------------------------------------------------------- reduce
@@ -1426,36 +762,7 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a) {
   finish_solve_iteration(ctl, prm, k, theta, eta, rp, a.cert_follows, a.cond, a.use_cond);
 }
 
-// ------------------------------------------------------------- finalize
-// Single-GPU fusion of reduce + update: one cooperative launch (every CTA
-// co-resident) with one software grid barrier between the sums and the
-// recurrence. Row sums are read warp-per-row from the [row][stripe] partials
-// (coalesced), column sums thread-per-column from [group][col]. Every CTA folds
-// the per-CTA partials in the same order, so eta/shift agree bit-for-bit; the
-// last CTA to finish applies the stopping logic (solver.cpp:179-235).
-struct FinalizeArgs {
-  const double* rowpart;  // [m][stripes]
-  const double* colpart;  // [groups][ld]
-  const double* p;
-  const double* q;
-  double* r;
-  double* s;
-  double* phi;
-  double* psi;
-  double* a;
-  double* b;
-  double* S;              // column sums scratch [n]
-  double* part;           // [gridDim.x * 3]
-  double* part2;          // [gridDim.x]
-  const Params* prm;
-  Ctl* ctl;
-  long long m, n, ld;
-  int stripes, groups;
-  cudaGraphConditionalHandle cond;
-  int use_cond;
-  int cert_follows;
-};
-
+// ------------------------------------------------------------ grid barrier
 __device__ __forceinline__ void grid_barrier(unsigned long long* counter) {
   // Arrival number a belongs to generation a / gridDim.x; wait until the
   // counter reaches the end of that generation (one atomic + one polled word).
@@ -1478,96 +785,6 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* counter) {
 __device__ void finish_solve_iteration(Ctl* ctl, const Params& prm, long long k, double theta,
                                        double eta, double rp, int cert_follows,
                                        cudaGraphConditionalHandle cond, int use_cond);
-
-__global__ void __launch_bounds__(kThreads) finalize_kernel(FinalizeArgs a) {
-  Ctl* ctl = a.ctl;
-  if (ctl->done) return;  // grid-uniform
-  const Params& prm = *a.prm;
-  __shared__ double red[kWarps];
-  __shared__ double sc[3];
-  __shared__ bool last;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long gwarp = (long long)blockIdx.x * kWarps + warp;
-  const long long nwarps = (long long)gridDim.x * kWarps;
-  // phase 1: rows (warp per row)
-  double sr = 0.0, sr2 = 0.0, sR = 0.0;
-  for (long long i = gwarp; i < a.m; i += nwarps) {
-    double R = 0.0;
-    for (int t = lane; t < a.stripes; t += 32) R += a.rowpart[i * a.stripes + t];
-    R = warp_sum(R);
-    const double ri = R - a.p[i];
-    if (lane == 0) a.r[i] = ri;
-    sr += ri;
-    sr2 += ri * ri;
-    sR += R;
-  }
-  // columns (thread per column, same mapping reused in phase 2)
-  const long long tid = (long long)blockIdx.x * kThreads + threadIdx.x;
-  const long long nthr = (long long)gridDim.x * kThreads;
-  for (long long j = tid; j < a.n; j += nthr) {
-    double S = 0.0;
-    for (int g = 0; g < a.groups; ++g) S += a.colpart[(long long)g * a.ld + j];
-    a.S[j] = S;
-  }
-  // lane 0 of each warp holds that warp's row sums (all lanes hold the same)
-  const double t1 = block_sum(lane == 0 ? sr : 0.0, red);
-  const double t2 = block_sum(lane == 0 ? sr2 : 0.0, red);
-  const double t3 = block_sum(lane == 0 ? sR : 0.0, red);
-  if (threadIdx.x == 0) {
-    a.part[blockIdx.x * 3 + 0] = t1;
-    a.part[blockIdx.x * 3 + 1] = t2;
-    a.part[blockIdx.x * 3 + 2] = t3;
-  }
-  grid_barrier(&ctl->bar_fin);
-  if (threadIdx.x == 0) {
-    double u1 = 0.0, u2 = 0.0, u3 = 0.0;
-    for (unsigned c = 0; c < gridDim.x; ++c) {
-      u1 += __ldcg(a.part + c * 3 + 0);
-      u2 += __ldcg(a.part + c * 3 + 1);
-      u3 += __ldcg(a.part + c * 3 + 2);
-    }
-    sc[0] = u1;
-    sc[1] = u2;
-    sc[2] = u3;
-  }
-  __syncthreads();
-  const long long k = ctl->k;
-  const double theta = ctl->theta[k & 1];
-  const double mn = (double)(a.m + a.n);
-  const double eta = __ddiv_rn(sc[0], mn);
-  const double shift = __dsub_rn(2.0 * eta, theta);
-  const double dn = (double)a.n, dm = (double)a.m;
-  // phase 2: recurrence (solver.cpp:28-37)
-  for (long long i = tid; i < a.m; i += nthr) {
-    const double ri = __ldcg(a.r + i), ai = a.a[i];
-    a.phi[i] = __ddiv_rn(__dadd_rn(__dsub_rn(ai, 2.0 * ri), shift), dn);
-    a.a[i] = __dsub_rn(ai, ri);
-  }
-  double ssq = 0.0;
-  for (long long j = tid; j < a.n; j += nthr) {
-    const double sj = __dsub_rn(a.S[j], a.q[j]);
-    const double bj = a.b[j];
-    a.s[j] = sj;
-    a.psi[j] = __ddiv_rn(__dadd_rn(__dsub_rn(bj, 2.0 * sj), shift), dm);
-    a.b[j] = __dsub_rn(bj, sj);
-    ssq += sj * sj;
-  }
-  const double bs = block_sum(ssq, red);
-  if (threadIdx.x == 0) {
-    a.part2[blockIdx.x] = bs;
-    __threadfence();
-    last = atomicAdd(&ctl->cnt_update, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!last || threadIdx.x != 0) return;
-  __threadfence();
-  double tssq = 0.0;
-  for (unsigned c = 0; c < gridDim.x; ++c) tssq += __ldcg(a.part2 + c);
-  ctl->cnt_update = 0;
-  const double nr = sqrt(sc[1]), ns = sqrt(tssq);
-  const double rp = (nr < ns) ? ns : nr;  // std::max semantics (solver.cpp:179)
-  finish_solve_iteration(ctl, prm, k, theta, eta, rp, a.cert_follows, a.cond, a.use_cond);
-}
 
 // ------------------------------------------------------ certificate / objective
 // duality.cpp:9-24 + problem.cpp:76-85. Tiled like the group-lasso sweep (one

@@ -371,13 +371,13 @@ def test_large_fp32_properties(ora):
     np.testing.assert_allclose(g.X.sum(axis=1) - p, g.r, atol=1e-9)
 
 
-@pytest.mark.parametrize("kernel", ["auto", "pipe", "ring", "stage", "cluster", "twopass"])
+@pytest.mark.parametrize("kernel", ["auto", "twopass"])
 @pytest.mark.parametrize("storage,m,n,classes", [
-    ("f64", 3000, 300, 2),    # long segments: cluster of 8 CTAs (DSMEM norms)
+    ("f64", 3000, 300, 2),    # 1500-row class segments
     ("f32", 3000, 301, 2),
     ("f32", 1000, 1000, 10),  # the cfg3 shape at 1/10 scale
-    ("f64", 2000, 203, 2),    # 1000-row segments: TMA box ring / segment-staged
-    ("f64", 4000, 64, 1),     # segment too long for any staging: two-phase fallback
+    ("f64", 2000, 203, 2),    # 1000-row segments
+    ("f64", 4000, 64, 1),     # segment too long for the pipeline's staging: two-phase kernel
 ])
 def test_gl_long_segments_match_oracle(ora, monkeypatch, kernel, storage, m, n, classes):
     if kernel != "auto":
@@ -599,28 +599,6 @@ def test_otpb_device_io(ora, tmp_path, storage):
         eng.read_cost_otpb(cpath, p, q)
     eng.close()
     ref.close()
-
-
-@pytest.mark.parametrize("storage", ["f64", "f32"])
-def test_tma_sweep_matches_register_sweep(ora, monkeypatch, storage):
-    """OTDR_SWEEP=tma (TMA ring) and the register-staged sweep give identical
-    iterates (same element-wise arithmetic and partial layout)."""
-    m, n = 1300, 1111
-    C, p, q, *_ = ora.gaussian_problem(m, n, 6)
-    outs = []
-    for mode in ("tma", "regs"):
-        monkeypatch.setenv("OTDR_SWEEP", mode)
-        monkeypatch.setenv("OTDR_RESIDENT", "off")
-        monkeypatch.setenv("OTDR_STREAM", "off")
-        eng = otdr.Engine(m, n, storage)
-        eng.set_problem(C, p, q)
-        eng.set_regularizer(otdr.QuadraticReg(12.0))
-        eng.set_state()
-        eng.step(otdr.default_stepsize(m, n), 20)
-        outs.append(eng.get_state())
-        eng.close()
-    a, b = outs
-    assert np.array_equal(a.X, b.X) and np.array_equal(a.phi, b.phi) and np.array_equal(a.psi, b.psi)
 
 
 @pytest.mark.parametrize("m,n", [(1, 1), (5, 3000), (33, 257), (300, 517), (1500, 1400), (2100, 700)])
