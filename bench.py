@@ -435,7 +435,7 @@ def run_ours(args):
         achieved = bytes_per_launch / (ms * 1e-3) / 1e9
         # the committed ncu capture is of the unsharded plan: no per-band figure
         tr = ncu_traffic("stream") if world == 1 else None
-        roof = {"kernel": "stream_kernel (persistent solve: sweep + partial folds + recurrence, "
+        roof = {"kernel": f"{eng.kernel_name()} (persistent solve: sweep + partial folds + recurrence, "
                           f"one launch for all {args.steps} timed iterations)",
                 "bytes_per_launch": bytes_per_launch, "launch_ms": ms,
                 "traffic": tr * args.steps if tr else None}

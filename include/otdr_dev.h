@@ -219,6 +219,10 @@ int otdr_dev_kernels_per_iteration(const otdr_dev* ctx);
  * (no certificate / trace / fused): OTDR_PATH_* below. */
 enum { OTDR_PATH_GRAPH = 0, OTDR_PATH_RESIDENT = 1, OTDR_PATH_STREAM = 2 };
 int otdr_dev_solve_path(const otdr_dev* ctx);
+/* Human-readable name of the kernel step()/solve() launch in the current
+ * configuration (e.g. "stream_kernel<f32, quad, sign-screened>"), for logs and
+ * benchmark records; the string lives as long as the context. */
+const char* otdr_dev_kernel_name(const otdr_dev* ctx);
 
 /* ---------------------------------------------------------------- batched
  * B independent problems of one shape solved by ONE launch, each problem owned

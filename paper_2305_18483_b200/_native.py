@@ -68,7 +68,7 @@ EXPORTS = [
     "otdr_dev_set_regularizer", "otdr_dev_set_state", "otdr_dev_load_state", "otdr_dev_step",
     "otdr_dev_solve", "otdr_dev_get_state", "otdr_dev_objective", "otdr_dev_duality_gap",
     "otdr_dev_get_trace", "otdr_dev_profile", "otdr_dev_time_steps",
-    "otdr_dev_kernels_per_iteration", "otdr_dev_solve_path", "otdr_dev_peer_export",
+    "otdr_dev_kernels_per_iteration", "otdr_dev_solve_path", "otdr_dev_kernel_name", "otdr_dev_peer_export",
     "otdr_dev_peer_import", "otdr_dev_peer_link_local", "otdr_dev_read_cost_otpb", "otdr_dev_write_plan_otpb",
     "otdr_batch_create", "otdr_batch_destroy", "otdr_batch_last_error", "otdr_batch_set_problems",
     "otdr_batch_build_sqdist_costs", "otdr_batch_set_regularizer", "otdr_batch_solve",
@@ -136,6 +136,8 @@ def lib():
     L.otdr_dev_kernels_per_iteration.restype = ct.c_int
     L.otdr_dev_solve_path.argtypes = [vp]
     L.otdr_dev_solve_path.restype = ct.c_int
+    L.otdr_dev_kernel_name.argtypes = [vp]
+    L.otdr_dev_kernel_name.restype = ct.c_char_p
     L.otdr_dev_peer_export.argtypes = [vp, ct.c_char_p]
     L.otdr_dev_peer_export.restype = ct.c_int
     L.otdr_dev_peer_import.argtypes = [vp, ct.c_char_p]

@@ -286,13 +286,12 @@ struct otdr_dev {
   size_t str_part_cap = 0;
   double *str_part = nullptr, *str_colpart = nullptr;
   int str_big = 1, str_small = 1, str_head = 0;
-  // streaming kernel (fp32 storage): 2 = warp-private bulk-copy rings
-  // (wstream_kernel, default), 1 = TMA producer warp + consumer warps
-  // (tstream_kernel, OTDR_STREAM_KERNEL=tma), 0 = per-thread cp.async queues
-  // (stream_kernel, OTDR_STREAM_KERNEL=async; always for fp64 storage);
-  // ts_cfg picks the tstream consumer geometry
-  int str_kind = 2, ts_cfg = 0;
-  bool screen = true;  // fp32 sign screen in the TMA kernel (OTDR_SCREEN=0: dense sweep)
+  // streaming kernel: 1 = TMA producer warp + consumer warps (tstream_kernel,
+  // the fp32-storage default), 0 = per-thread cp.async queues (stream_kernel;
+  // fp64 storage, and fp32 with OTDR_STREAM_KERNEL=async); ts_cfg picks the
+  // tstream consumer geometry
+  int str_kind = 1, ts_cfg = 0;
+  std::string kname;  // otdr_dev_kernel_name
   CUtensorMap ts_mapX{}, ts_mapC{};
   bool ts_maps = false;
   int* d_sfirst = nullptr;
@@ -659,24 +658,6 @@ struct otdr_dev {
 
   void check_launch() { CK(cudaGetLastError()); }
 
-  // max C_ij of the stored cost -> prm.cmax (the streaming kernel's fp32 sign
-  // screen is exact only with this bound; 0 disables it)
-  void refresh_cmax() {
-    CK(cudaMemsetAsync(d_mx, 0, 8, stream));
-    const long long cnt = m_loc * ld;
-    if (cnt > 0) {
-      if (f64()) otdrk::cmax_kernel<double><<<4 * kNumSMs, 256, 0, stream>>>((const double*)C, cnt, d_mx);
-      else otdrk::cmax_kernel<float><<<4 * kNumSMs, 256, 0, stream>>>((const float*)C, cnt, d_mx);
-      check_launch();
-    }
-    unsigned long long bits = 0;
-    CK(cudaMemcpyAsync(&bits, d_mx, 8, cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    double mx;
-    std::memcpy(&mx, &bits, 8);
-    prm.cmax = (std::isfinite(mx) && mx > 0.0) ? mx : 0.0;
-    push_prm();
-  }
 
   // ---------------------------------------------------------------- geometry
   void plan_geometry() {
@@ -766,8 +747,7 @@ struct otdr_dev {
     int occ = 0;
     if (str_d < 0) str_d = default_stream_d();
     cudaLaunchConfig_t lc{};
-    if (use_wstream()) wstream_dispatch(lc, otdrk::StreamArgs{}, &occ);
-    else if (use_tstream()) tstream_dispatch(lc, otdrk::StreamArgs{}, &occ);
+    if (use_tstream()) tstream_dispatch(lc, otdrk::StreamArgs{}, &occ);
     else stream_dispatch(lc, otdrk::StreamArgs{}, &occ);
     if (occ < 1) return;
     long long P = (long long)num_sms * occ;
@@ -845,8 +825,10 @@ struct otdr_dev {
   void stream_call(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
     constexpr bool E = sizeof(T) == 8;
     constexpr int NV = E ? 4 : 2, U = E ? 1 : 2;
-    auto kern = otdrk::stream_kernel<T, REG, E, NV, U, D>;
-    const size_t smem = stream_smem_of<T, REG, D>();
+    stream_launch(otdrk::stream_kernel<T, REG, E, NV, U, D>, stream_smem_of<T, REG, D>(), lc, sa, occ);
+  }
+  template <typename K>
+  void stream_launch(K kern, size_t smem, cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     if (occ) {
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, otdrk::kThreads, smem));
@@ -880,17 +862,11 @@ struct otdr_dev {
   // geometry (consumer warps, rows per block, ring stages): fp32 8/16/5,
   // fp64 8/8/5 (~187 KB of shared memory, one CTA per SM); OTDR_TS_CFG=1
   // selects 16 consumer warps
-  int ts_rb() const { return ts_cfg == 1 || ts_cfg == 2 ? 16 : 8; }
-  // the fp32 sign screen (ts_consume_sparse) needs the cost bound and rho,
-  // rho * cmax inside the fp32 normal range
-  bool ts_sparse() const {
-    const double r = prm.rho, rc = prm.rho * prm.cmax;
-    return screen && prm.cmax > 0.0 && r > 1e-30 && r < 1e30 && rc > 1e-30 && rc < 1e30;
-  }
-  template <typename T, int REG, int NCW, int RB, int S, int MINB, bool SP>
+  int ts_rb() const { return ts_cfg == 1 ? 16 : 8; }
+  template <typename T, int REG, int NCW, int RB, int S, int MINB>
   void tstream_call(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
     constexpr bool E = sizeof(T) == 8;
-    auto kern = otdrk::tstream_kernel<T, REG, E, NCW, RB, S, MINB, false, SP>;
+    auto kern = otdrk::tstream_kernel<T, REG, E, NCW, RB, S, MINB>;
     constexpr size_t smem = otdrk::TSLayout<T, NCW, RB, S>::kBytes;
     constexpr int nt = (NCW + 1) * 32;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -912,16 +888,8 @@ struct otdr_dev {
     // fp32: two CTAs per SM of 8 consumer warps (one row per warp per block)
     // + a producer warp, 5-stage ring of 8-row blocks (~106 KB per CTA);
     // OTDR_TS_CFG=1: one CTA of 16 consumer warps, 16-row blocks
-    if (ts_cfg == 1) {
-      if (ts_sparse()) tstream_call<T, REG, 16, 16, 5, 1, true>(lc, sa, occ);
-      else tstream_call<T, REG, 16, 16, 5, 1, false>(lc, sa, occ);
-    } else if (ts_cfg == 2) {  // one CTA per SM: 8 warps x 2 rows, 6-stage ring of 16-row blocks
-      if (ts_sparse()) tstream_call<T, REG, 8, 16, 6, 1, true>(lc, sa, occ);
-      else tstream_call<T, REG, 8, 16, 6, 1, false>(lc, sa, occ);
-    } else {
-      if (ts_sparse()) tstream_call<T, REG, 8, 8, 5, 2, true>(lc, sa, occ);
-      else tstream_call<T, REG, 8, 8, 5, 2, false>(lc, sa, occ);
-    }
+    if (ts_cfg == 1) tstream_call<T, REG, 16, 16, 5, 1>(lc, sa, occ);
+    else tstream_call<T, REG, 8, 8, 5, 2>(lc, sa, occ);
   }
   void tstream_dispatch(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
     const bool quad = reg_kind == OTDR_REG_QUAD;
@@ -931,33 +899,6 @@ struct otdr_dev {
   // the bulk-copy kernels cover fp32 storage; fp64 rows (2 KB per 256
   // columns) keep the per-thread cp.async kernel
   bool use_tstream() const { return str_kind == 1 && !f64(); }
-  bool use_wstream() const { return str_kind == 2 && !f64(); }
-
-  // ---- warp-private bulk-copy rings (wstream_kernel, the fp32 default)
-  static constexpr int kWSD = 5;  // rows in flight per warp
-  template <int REG, bool SP>
-  void wstream_call(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
-    auto kern = otdrk::wstream_kernel<REG, otdrk::kWarps, kWSD, SP>;
-    constexpr size_t smem = otdrk::WSLayout<REG, otdrk::kWarps, kWSD>::kBytes;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    if (occ) {
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, otdrk::kThreads, smem));
-      return;
-    }
-    lc.blockDim = dim3(unsigned(otdrk::kThreads), 1, 1);
-    lc.dynamicSmemBytes = smem;
-    CK(cudaLaunchKernelEx(&lc, kern, sa));
-  }
-  void wstream_dispatch(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
-    const bool quad = reg_kind == OTDR_REG_QUAD, sp = ts_sparse();
-    if (quad) {
-      if (sp) wstream_call<otdrk::REG_QUAD, true>(lc, sa, occ);
-      else wstream_call<otdrk::REG_QUAD, false>(lc, sa, occ);
-    } else {
-      if (sp) wstream_call<otdrk::REG_NONE, true>(lc, sa, occ);
-      else wstream_call<otdrk::REG_NONE, false>(lc, sa, occ);
-    }
-  }
 
   bool stream_active(bool track, bool cert) const {
     return str_P > 0 && res_G == 0 && !track && !cert && (!prm.fused || str_d > 0);
@@ -988,8 +929,7 @@ struct otdr_dev {
     attr[0].val.cooperative = 1;
     lc.attrs = attr;
     lc.numAttrs = 1;
-    if (use_wstream()) wstream_dispatch(lc, sa, nullptr);
-    else if (use_tstream()) tstream_dispatch(lc, sa, nullptr);
+    if (use_tstream()) tstream_dispatch(lc, sa, nullptr);
     else stream_dispatch(lc, sa, nullptr);
     if (trace) {  // debug: per-iteration phase times of the first iterations
       std::vector<unsigned long long> h(tsn);
@@ -1469,6 +1409,21 @@ int otdr_dev_solve_path(const otdr_dev* ctx) {
   return OTDR_PATH_GRAPH;
 }
 
+const char* otdr_dev_kernel_name(const otdr_dev* ctx) {
+  if (!ctx) return "";
+  otdr_dev* c = const_cast<otdr_dev*>(ctx);
+  const char* st = c->f64() ? "f64" : "f32";
+  const char* rg = c->reg_kind == OTDR_REG_QUAD ? "quad" : c->reg_kind == OTDR_REG_GROUP_LASSO ? "group-lasso" : "none";
+  const int path = otdr_dev_solve_path(ctx);
+  if (path == OTDR_PATH_RESIDENT) c->kname = std::string("resident_kernel<") + st + ", " + rg + ">";
+  else if (path == OTDR_PATH_STREAM && c->reg_kind == OTDR_REG_GROUP_LASSO)
+    c->kname = std::string("gl_stream_kernel<") + st + ">";
+  else if (path == OTDR_PATH_STREAM) {
+    c->kname = std::string(c->use_tstream() ? "tstream_kernel" : "stream_kernel") + "<" + st + ", " + rg + ">";
+  } else c->kname = std::string("sweep + reduce + update graph<") + st + ", " + rg + ">";
+  return c->kname.c_str();
+}
+
 otdr_status otdr_dev_peer_export(otdr_dev* ctx, void* handle) {
   if (!ctx || !handle) return OTDR_E_INVALID_ARG;
   return guarded(ctx, [&] {
@@ -1629,10 +1584,8 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     if (const char* tp = std::getenv("OTDR_STREAM_TILES")) ctx->str_tpc = std::max(1, std::atoi(tp));
     if (const char* tl = std::getenv("OTDR_STREAM_TAIL")) ctx->str_tail = std::max(1, std::atoi(tl));
     if (const char* sd = std::getenv("OTDR_STREAM_D")) ctx->str_d = std::atoi(sd);
-    if (const char* sk = std::getenv("OTDR_STREAM_KERNEL"))
-      ctx->str_kind = std::strcmp(sk, "async") == 0 ? 0 : std::strcmp(sk, "tma") == 0 ? 1 : 2;
+    if (const char* sk = std::getenv("OTDR_STREAM_KERNEL")) ctx->str_kind = std::strcmp(sk, "async") == 0 ? 0 : 1;
     if (const char* tc = std::getenv("OTDR_TS_CFG")) ctx->ts_cfg = std::atoi(tc);
-    ctx->screen = !(std::getenv("OTDR_SCREEN") && std::strcmp(std::getenv("OTDR_SCREEN"), "0") == 0);
     ctx->plan_geometry();
     ctx->bpart = dalloc<double>(size_t(ctx->RB + ctx->CB) * 3);
     ctx->csum = dalloc<double>(otdrk::kCertVals);
@@ -1692,7 +1645,6 @@ otdr_status otdr_dev_set_problem(otdr_dev* ctx, const double* cost_rm, const dou
     else ctx->upload_rows<float>((float*)ctx->C, cost_rm);
     ctx->upload_vec_rows(ctx->p, p);
     CK(cudaMemcpy(ctx->q, q, size_t(ctx->n) * 8, cudaMemcpyHostToDevice));
-    ctx->refresh_cmax();
     ctx->has_problem = true;
     ctx->has_state = false;
     return OTDR_OK;
@@ -1743,7 +1695,6 @@ otdr_status otdr_dev_build_sqdist_cost(otdr_dev* ctx, const double* src_pts,
     ctx->h_q.assign(q, q + ctx->n);
     ctx->upload_vec_rows(ctx->p, p);
     CK(cudaMemcpy(ctx->q, q, size_t(ctx->n) * 8, cudaMemcpyHostToDevice));
-    ctx->refresh_cmax();
     ctx->has_problem = true;
     ctx->has_state = false;
     return OTDR_OK;
@@ -1832,7 +1783,6 @@ otdr_status otdr_dev_read_cost_otpb(otdr_dev* ctx, const char* path, const doubl
     ctx->h_q.assign(q, q + ctx->n);
     ctx->upload_vec_rows(ctx->p, p);
     CK(cudaMemcpy(ctx->q, q, size_t(ctx->n) * 8, cudaMemcpyHostToDevice));
-    ctx->refresh_cmax();
     ctx->has_problem = true;
     ctx->has_state = false;
     return OTDR_OK;

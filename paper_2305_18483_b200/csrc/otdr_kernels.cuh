@@ -48,7 +48,6 @@ struct Params {
   int fused;
   int solving;      // stopping logic active (solve) vs raw step()
   long long trace_cap;
-  double cmax;      // max_ij C_ij of the stored cost (0: unknown -> no sign screen)
 };
 
 // Device control block: the solver's scalar state and loop bookkeeping.
@@ -996,24 +995,6 @@ __global__ void __launch_bounds__(kThreads) cert_final_kernel(CertFinalArgs a) {
 }
 
 // ---------------------------------------------------------------- utilities
-// max over the stored (non-negative) cost: the bound the streaming kernel's
-// fp32 sign screen needs (otdr_tstream.cuh). Non-negative IEEE values order
-// like their bit patterns, so an integer atomicMax suffices.
-template <typename T>
-__global__ void cmax_kernel(const T* C, long long count, unsigned long long* out) {
-  unsigned long long mx = 0;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < count;
-       t += (long long)gridDim.x * blockDim.x) {
-    const double v = (double)C[t];
-    const unsigned long long b = __double_as_longlong(v);
-    mx = (v > 0.0 && b > mx) ? b : mx;  // NaN / negative never win
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
-    mx = y > mx ? y : mx;
-  }
-  if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
-}
 __global__ void stamp_t0_kernel(Ctl* c) { c->t0_ns = globaltimer_ns(); }
 
 // Moves whole rows (16-byte units): dst row dst_row[h] <- src row src_row[h].

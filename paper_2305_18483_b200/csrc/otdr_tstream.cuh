@@ -78,20 +78,16 @@ struct TSLayout {
 // Column partial of a finished tile (fixed warp order) and the stripe fold of
 // the CTA completing the stripe -- stream_stripe_done for the NCW consumer
 // warps only (named barrier 1; the producer warp is elsewhere).
-// IN_SMEM: the warps' column partials already sit in red[warp][col] (the
-// sign-screened sweep accumulates them there) instead of registers.
-template <int NCW, int NV, int VEC, bool IN_SMEM = false>
+template <int NCW, int NV, int VEC>
 __device__ __forceinline__ void ts_flush(const StreamArgs& A, int tile, long long stripe,
                                          double (*cacc)[VEC], double* red, double* sred,
                                          int* s_last, int par, unsigned long long plast) {
   constexpr int NC = NCW * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if constexpr (!IN_SMEM) {
 #pragma unroll
-    for (int v = 0; v < NV; ++v)
+  for (int v = 0; v < NV; ++v)
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) red[warp * kStreamTN + v * 32 * VEC + lane * VEC + e] = cacc[v][e];
-  }
+    for (int e = 0; e < VEC; ++e) red[warp * kStreamTN + v * 32 * VEC + lane * VEC + e] = cacc[v][e];
   named_bar_sync(1, NC);
   if (threadIdx.x < kStreamTN) {
     double sum = 0.0;
@@ -257,167 +253,10 @@ __device__ __forceinline__ void ts_consume(const StreamArgs& A, unsigned char* s
   }
 }
 
-// ---------------------------------------------------------------------------
-// Sign-screened sweep (fp32 storage, plain mode). Once the plan settles, more
-// than 99 % of the entries clamp to zero, yet the dense sweep
-// spends two f32->f64 conversions, the fp64 chain and an f64->f32 conversion
-// on every one. Here each entry is first screened in fp32:
-//     t = fma(k, x, ((fma(-rho32, c, x) + phi') + psi'))
-// with phi' = phi32 + (k|phi32| + 2^-120), psi' = psi32 + k(|psi32| + rho32 cmax),
-// k = 2^-20. The fp32 evaluation of (x - rho c) + phi + psi is within
-// 2^-21 (x + rho c + |phi| + |psi|) of the real value (four roundings of
-// 2^-24 plus the conversions; 2^-120 covers subnormal steps), and the fp64
-// evaluation within 2^-51 of it, so t < 0 proves the fp64 value v < 0, i.e.
-// X_{k+1} = 0 exactly. NaN / inf operands never pass the screen. Every lane
-// then computes its unresolved entries (t >= 0: the non-zeros and a thin band
-// around them) with the dense kernel's exact fp64 expression (solver.cpp:97-100,
-// regularizers.cpp:54); entry slots no lane of the warp needs are skipped by a
-// warp vote. Screened entries contribute exact zeros to the row and column
-// sums, so stored plan, row partials and column partials are bit-identical to
-// the dense sweep's (same per-lane order, same butterfly). Padded columns
-// carry psi = -inf and screen to zero.
-template <int REG, int NCW, int RB, int S>
-__device__ __forceinline__ void ts_consume_sparse(const StreamArgs& A, unsigned char* smem, int& ring,
-                                                  unsigned& round, double* sred, int* s_last, int par,
-                                                  double rho, double qinv, double cmax) {
-  using LY = TSLayout<float, NCW, RB, S>;
-  constexpr int VEC = 4, NV = 2, RPW = RB / NCW;
-  const float* tiles = reinterpret_cast<const float*>(smem + LY::oTiles);
-  const double* psis = reinterpret_cast<const double*>(smem + LY::oPsi);
-  const double* phis = reinterpret_cast<const double*>(smem + LY::oPhi);
-  const TSMeta* meta = reinterpret_cast<const TSMeta*>(smem + LY::oMeta);
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + LY::oBar);
-  unsigned long long* empty = full + S;
-  double* red = reinterpret_cast<double*>(smem + LY::oRed);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned long long plast = policy_evict_last();
-  float* X = static_cast<float*>(A.X);
-  const float r32 = (float)rho, kS = 0x1p-20f;
-  const float rc32 = r32 * (float)cmax;
-  // column partials live in this warp's row of red (written only for
-  // unresolved entries: same per-column row order as the dense registers)
-  double* colw = red + warp * kStreamTN;
-  double psi_r[NV][VEC];
-  float psp[NV][VEC];
-  bool cok[NV];
-  float* xrow_base = X;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    cok[v] = false;
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      psi_r[v][e] = 0.0;
-      psp[v][e] = 0.f;
-    }
-  }
-  for (;;) {
-    mbar_wait(&full[ring], round);
-    const TSMeta md = meta[ring];
-    if (md.tile < 0) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[ring]);
-      if (++ring == S) {
-        ring = 0;
-        round ^= 1u;
-      }
-      return;
-    }
-    const long long stripe = md.stripe;
-    if (md.flags & kTSFirst) {
-      const double* ps = psis + (size_t)ring * kStreamTN;
-      xrow_base = X + stripe * kStreamTN;
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int cb = v * 32 * VEC + lane * VEC;
-        cok[v] = stripe * kStreamTN + cb < A.ld;
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const double pv = ps[cb + e];
-          const float p32 = (float)pv;
-          psi_r[v][e] = pv;
-          psp[v][e] = pv == -INFINITY ? -INFINITY : p32 + kS * (fabsf(p32) + rc32);
-        }
-        *reinterpret_cast<double2*>(colw + cb) = make_double2(0.0, 0.0);
-        *reinterpret_cast<double2*>(colw + cb + 2) = make_double2(0.0, 0.0);
-      }
-    }
-    const float* xt = tiles + (size_t)ring * 2 * RB * kStreamTN;
-    const float* ct = xt + RB * kStreamTN;
-    const double* ph_s = phis + (size_t)ring * RB;
-    double rs[RPW];
-#pragma unroll
-    for (int u = 0; u < RPW; ++u) {
-      const int t = warp + u * NCW;
-      rs[u] = 0.0;
-      if (t < md.nrows) {  // warp-uniform
-        const double ph = ph_s[t];
-        const float ph32 = (float)ph;
-        const float php = ph32 + (kS * fabsf(ph32) + 0x1p-120f);
-        const float* xr = xt + (size_t)t * kStreamTN;
-        const float* cr = ct + (size_t)t * kStreamTN;
-        float o[NV][VEC];
-        bool nd[NV][VEC];
-        bool anynd = false;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const float4 xv = reinterpret_cast<const float4*>(xr)[v * 32 + lane];
-          const float4 cv = reinterpret_cast<const float4*>(cr)[v * 32 + lane];
-          const float x[4] = {xv.x, xv.y, xv.z, xv.w}, c[4] = {cv.x, cv.y, cv.z, cv.w};
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            const float sc = fmaf(kS, x[e], (fmaf(-r32, c[e], x[e]) + php) + psp[v][e]);
-            nd[v][e] = !(sc < 0.f);
-            anynd |= nd[v][e];
-            o[v][e] = 0.f;
-          }
-        }
-        if (__any_sync(0xffffffffu, anynd)) {  // warp-uniform
-#pragma unroll
-          for (int v = 0; v < NV; ++v)
-#pragma unroll
-            for (int e = 0; e < VEC; ++e)
-              if (__any_sync(0xffffffffu, nd[v][e]) && nd[v][e]) {
-                // the dense sweep's expression (EXACT = false): ((X - rho C) + phi) + psi
-                const int col = v * 32 * VEC + lane * VEC + e;  // x, c re-read: rare path
-                const double val = (fma(-rho, (double)cr[col], (double)xr[col]) + ph) + psi_r[v][e];
-                double nx = clamp0(val);
-                if (REG == REG_QUAD) nx = nx * qinv;
-                o[v][e] = (float)nx;
-                colw[v * 32 * VEC + lane * VEC + e] += nx;  // this lane's own column
-                rs[u] += nx;
-              }
-          rs[u] = warp_sum(rs[u]);
-        }
-        float4* xg = reinterpret_cast<float4*>(xrow_base + (md.row0 + t) * A.ld);
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-          if (cok[v]) xg[v * 32 + lane] = make_float4(o[v][0], o[v][1], o[v][2], o[v][3]);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[ring]);  // the stage's shared memory is free
-    if (++ring == S) {
-      ring = 0;
-      round ^= 1u;
-    }
-#pragma unroll
-    for (int u = 0; u < RPW; ++u) {
-      const int t = warp + u * NCW;
-      if (lane == 0 && t < md.nrows)
-        st_hint(A.rowpart + (long long)(md.row0 + t) * A.stripes + stripe, rs[u], plast);
-    }
-    if (md.flags & kTSLast)
-      ts_flush<NCW, NV, VEC, true>(A, md.tile, stripe, nullptr, red, sred, s_last, par, plast);
-  }
-}
-
 // FUSED: the even/odd path (solver.cpp:127-177) -- a separate instantiation,
 // so the plain loop carries no mode branches (fp32 storage runs `fused` on the
 // plain loop: otdr_dev_solve)
-// SPARSE: the sign-screened sweep (fp32 storage; the host selects it when the
-// cost bound is known and rho, rho * cmax lie inside the fp32 normal range).
-template <typename T, int REG, bool EXACT, int NCW, int RB, int S, int MINB, bool FUSED = false,
-          bool SPARSE = false>
+template <typename T, int REG, bool EXACT, int NCW, int RB, int S, int MINB, bool FUSED = false>
 __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     tstream_kernel(StreamArgs A, const __grid_constant__ CUtensorMap mapX,
                    const __grid_constant__ CUtensorMap mapC) {
@@ -539,226 +378,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
           ts_consume<T, REG, EXACT, NCW, RB, S, MODE_EVEN>(A, ts_smem, ring, round, sred, &s_last, par, rho, qd, qinv);
         else
           ts_consume<T, REG, EXACT, NCW, RB, S, MODE_ODD>(A, ts_smem, ring, round, sred, &s_last, par, rho, qd, qinv);
-      } else if constexpr (SPARSE) {
-        ts_consume_sparse<REG, NCW, RB, S>(A, ts_smem, ring, round, sred, &s_last, par, rho, qinv, prm.cmax);
       } else {
         ts_consume<T, REG, EXACT, NCW, RB, S, MODE_NORMAL>(A, ts_smem, ring, round, sred, &s_last, par, rho, qd, qinv);
       }
       // this sweep's X stores are read by the next iteration's TMA (async proxy)
       fence_proxy_async_global();
     }
-    stamp(c);
-    if (stream_finish_iteration<NT>(A, prm, L, sred, bc, &ctl->bar_tst, stamp)) break;
-  }
-}
-
-// ===========================================================================
-// Warp-private bulk-copy rings (wstream_kernel): the default fp32 streaming
-// solve. Same tiles, tile claiming, folds and phases B / C as stream_kernel;
-// in phase A every warp owns the rows r0 + w, r0 + w + NCW, ... of the claimed
-// tile and streams them through its OWN D-slot shared-memory ring: lane 0
-// issues, per row, two 1-D bulk copies (cp.async.bulk, the row's 256-column
-// segment of X and of C) and one of the row's phi pair, completing on the
-// slot's mbarrier; the warp consumes the row (dense fp64 sweep, or the fp32
-// sign screen of ts_consume_sparse) and lane 0 refills the slot D rows ahead.
-// No cross-warp coupling inside a tile (a slow row delays only its own warp),
-// no per-thread copy queues (one elected lane issues three copies per row).
-template <int REG, int NCW, int D>
-struct WSLayout {
-  static constexpr size_t kSlot = 2 * kStreamTN * 4 + 16;                  // X row, C row, phi pair
-  static constexpr size_t kSlotPad = (kSlot + 127) / 128 * 128;
-  static constexpr size_t oRing = 0;                                        // NCW x D slots
-  static constexpr size_t oBar = oRing + size_t(NCW) * D * kSlotPad;       // NCW x D mbarriers
-  static constexpr size_t oRed = (oBar + size_t(NCW) * D * 8 + 127) / 128 * 128;
-  static constexpr size_t kBytes = oRed + size_t(NCW) * kStreamTN * 8;
-};
-
-template <int REG, int NCW, int D, bool SPARSE>
-__global__ void __launch_bounds__(NCW * 32, 2) wstream_kernel(StreamArgs A) {
-  using LY = WSLayout<REG, NCW, D>;
-  constexpr int NT = NCW * 32, VEC = 4, NV = 2;
-  Ctl* ctl = A.ctl;
-  if (ctl->done) return;  // grid-uniform
-  const Params& prm = *A.prm;
-  extern __shared__ __align__(128) unsigned char ws_smem[];
-  __shared__ double sred[NT / 32];
-  __shared__ double bc[4];
-  __shared__ int s_last;
-  __shared__ int s_tile;
-  const int c = (int)blockIdx.x, P = (int)gridDim.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned char* ring = ws_smem + LY::oRing + (size_t)warp * D * LY::kSlotPad;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(ws_smem + LY::oBar) + warp * D;
-  double* red = reinterpret_cast<double*>(ws_smem + LY::oRed);
-  // zero the ring once: the last stripe's copies fill only ld - col0 columns,
-  // and the tail must hold finite values (it clamps to 0 through psi = -inf)
-  for (size_t t = (size_t)lane; t < D * LY::kSlotPad / 16; t += 32)
-    reinterpret_cast<uint4*>(ring)[t] = make_uint4(0u, 0u, 0u, 0u);
-  if (lane == 0)
-    for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
-  fence_proxy_async_smem();  // the zeroed ring before any bulk copy into it
-  __syncthreads();
-
-  const double rho = prm.rho, qinv = prm.quad_inv;
-  StreamLoop L;
-  L.k = ctl->k;
-  L.theta = ctl->theta[L.k & 1];
-  L.best = ctl->best;
-  L.last_imp = ctl->last_improvement;
-  L.k0 = ctl->k0;
-  L.it = 0;
-  L.epoch = (A.peers != nullptr ? *A.xep : 0ull) + 1;
-  L.shifted = 0;
-  const long long m = A.m;
-  const unsigned long long plast = policy_evict_last();
-  float* X = static_cast<float*>(A.X);
-  const float* Cm = static_cast<const float*>(A.C);
-  const float r32 = (float)rho, kS = 0x1p-20f;
-  const float rc32 = r32 * (float)prm.cmax;
-  unsigned long long q = 0;  // rows this warp has consumed (slot = q % D, parity = (q / D) & 1)
-  auto stamp = [&](int slot) {
-    if (A.tstamp && L.it < kTraceIters && threadIdx.x == 0 && (slot < P ? true : c == 0))
-      A.tstamp[L.it * (P + 12) + slot] = globaltimer_ns();
-  };
-
-  for (;;) {
-    stamp(P + 0);
-    // generic-proxy writes of the previous iteration (X, phi) before this
-    // iteration's bulk copies (async proxy); ordered by the grid barrier
-    fence_proxy_async_global();
-    for (;;) {
-      if (threadIdx.x == 0) s_tile = (int)atomicAdd(&ctl->tile_ctr, 1u);
-      __syncthreads();
-      const int tile = s_tile;
-      __syncthreads();  // s_tile read by every thread before the next claim
-      if (tile >= A.ntiles) break;
-      int st_, k_, R_;
-      const int hb = A.head * A.nb;
-      if (tile < hb) {
-        st_ = tile / A.nb;
-        k_ = tile - st_ * A.nb;
-        R_ = A.big;
-      } else {
-        const int t2 = tile - hb;
-        const int q2 = t2 / A.ns;
-        st_ = A.head + q2;
-        k_ = t2 - q2 * A.ns;
-        R_ = A.small;
-      }
-      const long long r0 = (long long)k_ * R_;
-      const long long r1 = (r0 + R_ < m) ? r0 + R_ : m;
-      const long long col0 = (long long)st_ * kStreamTN;
-      const unsigned seg = (unsigned)((A.ld - col0 < kStreamTN ? A.ld - col0 : kStreamTN) * 4);
-      auto issue = [&](long long i, unsigned long long qq) {  // lane 0
-        const int slot = int(qq % D);
-        unsigned char* sl = ring + (size_t)slot * LY::kSlotPad;
-        mbar_expect_tx(&bars[slot], 2 * seg + 16);
-        bulk_load(sl, X + i * A.ld + col0, seg, &bars[slot]);
-        bulk_load(sl + kStreamTN * 4, Cm + i * A.ld + col0, seg, &bars[slot]);
-        bulk_load(sl + 2 * kStreamTN * 4, A.phi + (i & ~1LL), 16, &bars[slot]);
-      };
-      // this warp's rows: r0 + warp + j * NCW
-      const long long first = r0 + warp;
-      const long long nrow = first < r1 ? (r1 - first + NCW - 1) / NCW : 0;
-      if (lane == 0)
-        for (long long j = 0; j < nrow && j < D; ++j) issue(first + j * NCW, q + j);
-      // tile constants: psi (fp64) and the screen's psi' per lane column
-      double psi_r[NV][VEC];
-      float psp[NV][VEC];
-      bool cok[NV];
-      double cacc[NV][VEC];
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const long long cb = col0 + v * 32 * VEC + lane * VEC;
-        cok[v] = cb < A.ld;
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const double pv = __ldcg(A.psi + cb + e);  // psi covers whole stripes (-inf padding)
-          psi_r[v][e] = pv;
-          const float p32 = (float)pv;
-          psp[v][e] = pv == -INFINITY ? -INFINITY : p32 + kS * (fabsf(p32) + rc32);
-          cacc[v][e] = 0.0;
-        }
-      }
-      for (long long j = 0; j < nrow; ++j) {
-        const long long i = first + j * NCW;
-        const int slot = int(q % D);
-        mbar_wait(&bars[slot], unsigned((q / D) & 1ull));
-        const unsigned char* sl = ring + (size_t)slot * LY::kSlotPad;
-        const float* xr = reinterpret_cast<const float*>(sl);
-        const float* cr = reinterpret_cast<const float*>(sl + kStreamTN * 4);
-        const double ph = reinterpret_cast<const double*>(sl + 2 * kStreamTN * 4)[i & 1];
-        float o[NV][VEC];
-        double rs = 0.0;
-        if constexpr (SPARSE) {
-          const float ph32 = (float)ph;
-          const float php = ph32 + (kS * fabsf(ph32) + 0x1p-120f);
-          bool nd[NV][VEC];
-          bool anynd = false;
-#pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            const float4 xv = reinterpret_cast<const float4*>(xr)[v * 32 + lane];
-            const float4 cv = reinterpret_cast<const float4*>(cr)[v * 32 + lane];
-            const float x[4] = {xv.x, xv.y, xv.z, xv.w}, cc[4] = {cv.x, cv.y, cv.z, cv.w};
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-              const float sc = fmaf(kS, x[e], (fmaf(-r32, cc[e], x[e]) + php) + psp[v][e]);
-              nd[v][e] = !(sc < 0.f);
-              anynd |= nd[v][e];
-              o[v][e] = 0.f;
-            }
-          }
-          if (__any_sync(0xffffffffu, anynd)) {
-#pragma unroll
-            for (int v = 0; v < NV; ++v)
-#pragma unroll
-              for (int e = 0; e < VEC; ++e)
-                if (__any_sync(0xffffffffu, nd[v][e]) && nd[v][e]) {
-                  const int col = v * 32 * VEC + lane * VEC + e;
-                  const double val = (fma(-rho, (double)cr[col], (double)xr[col]) + ph) + psi_r[v][e];
-                  double nx = clamp0(val);
-                  if (REG == REG_QUAD) nx = nx * qinv;
-                  o[v][e] = (float)nx;
-                  cacc[v][e] += nx;
-                  rs += nx;
-                }
-            rs = warp_sum(rs);
-          }
-        } else {
-#pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            double x[VEC], cc[VEC];
-            unpack(reinterpret_cast<const float4*>(xr)[v * 32 + lane], x);
-            unpack(reinterpret_cast<const float4*>(cr)[v * 32 + lane], cc);
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-              double nx = clamp0((fma(-rho, cc[e], x[e]) + ph) + psi_r[v][e]);  // solver.cpp:97-99
-              if (REG == REG_QUAD) nx = nx * qinv;                              // regularizers.cpp:54
-              o[v][e] = (float)nx;
-              cacc[v][e] += nx;
-              rs += nx;
-            }
-          }
-          rs = warp_sum(rs);
-        }
-        __syncwarp();  // every lane is done with the slot
-        if (lane == 0) {
-          if (j + D < nrow) {
-            fence_proxy_async_smem();  // the slot's generic reads before the async refill
-            issue(i + (long long)D * NCW, q + D);
-          }
-          st_hint(A.rowpart + i * (long long)A.stripes + st_, rs, plast);
-        }
-        ++q;
-        float4* xg = reinterpret_cast<float4*>(X + i * A.ld + col0);
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-          if (cok[v]) xg[v * 32 + lane] = make_float4(o[v][0], o[v][1], o[v][2], o[v][3]);
-      }
-      ts_flush<NCW, NV, VEC>(A, tile, st_, cacc, red, sred, &s_last, int(L.epoch & 1), plast);
-    }
-    // this sweep's X stores are read by the next iteration's bulk copies
-    fence_proxy_async_global();
     stamp(c);
     if (stream_finish_iteration<NT>(A, prm, L, sred, bc, &ctl->bar_tst, stamp)) break;
   }

@@ -604,6 +604,10 @@ class Engine:
         """Device loop used by step()/solve(): "graph", "resident" or "stream"."""
         return ("graph", "resident", "stream")[self._L.otdr_dev_solve_path(self._h)]
 
+    def kernel_name(self) -> str:
+        """The kernel step()/solve() launch in the current configuration."""
+        return self._L.otdr_dev_kernel_name(self._h).decode()
+
 
 def link_local(engines) -> None:
     """Link the rank contexts of ONE process (engines[r] = rank r) for the

@@ -1068,35 +1068,44 @@ def test_tol_gap_on_persistent_kernels(ora, monkeypatch, kind, param, tol_gap):
     assert abs(rep.objective - o.objective) <= 1e-10 * abs(o.objective)
 
 
-@pytest.mark.parametrize("m,n,alpha", [(3000, 2501, 13.0), (700, 4100, 1e7), (257, 300, 0.0)])
-def test_sign_screened_sweep_matches_dense_sweep(ora, monkeypatch, m, n, alpha):
-    """The fp32 sign screen of the TMA streaming kernel (ts_consume_sparse)
-    against the dense sweep (OTDR_SCREEN=0): bit-identical iterates -- the
-    screen only skips entries whose fp64 value is provably negative, the
-    unresolved ones use the dense expression, and the row / column partials
-    keep the dense summation order. alpha = 1e7 makes the plan dense
-    (every entry unresolved: several queue passes per row); alpha = 0 is the
-    unregularized path; n = 2501 / 4100 / 300 exercise the padded columns."""
-    C, p, q, *_ = ora.gaussian_problem(m, n, 4)
-    reg = otdr.QuadraticReg(alpha) if alpha > 0 else otdr.ZeroReg()
-    out = {}
-    for mode in ("1", "0"):
-        monkeypatch.setenv("OTDR_SCREEN", mode)
-        monkeypatch.setenv("OTDR_RESIDENT", "off")
-        eng = otdr.Engine(m, n, "f32")
-        eng.set_problem(C, p, q)
-        eng.set_regularizer(reg)
-        eng.set_state()
-        assert eng.solve_path() == "stream"
-        rho = otdr.default_stepsize(m, n)
-        eng.step(rho, 1)
-        s1 = eng.get_state()
-        eng.step(rho, 49)
-        s50 = eng.get_state()
-        eng.close()
-        out[mode] = (s1, s50)
-    (a1, a50), (b1, b50) = out["1"], out["0"]
-    for nm in ("X", "phi", "psi", "a", "b", "r", "s"):
-        assert np.array_equal(getattr(a1, nm), getattr(b1, nm)), nm
-        assert np.array_equal(getattr(a50, nm), getattr(b50, nm)), nm
-    assert a50.theta == b50.theta
+@pytest.mark.parametrize("kernel", ["tma", "async"])
+@pytest.mark.parametrize("m,n", [(3, 4000), (5, 3000), (33, 257), (300, 517), (1500, 1400), (2100, 2501)])
+@pytest.mark.parametrize("kind,param", [("none", 0.0), ("quad", 0.7)])
+def test_fp32_stream_kernels_match_oracle(ora, monkeypatch, kernel, m, n, kind, param):
+    """fp32 storage through both persistent streaming kernels -- the TMA
+    producer-warp kernel (tstream_kernel, the default: 8-row blocks, so m < 8
+    and tiles ending mid-block are covered) and the per-thread cp.async kernel
+    -- against the oracle on the fp32-rounded cost: iterates after k steps
+    within 1e-5, then a full solve (same termination, iterations within 2,
+    objective within 1e-6)."""
+    monkeypatch.setenv("OTDR_RESIDENT", "off")
+    monkeypatch.setenv("OTDR_STREAM_KERNEL", kernel)
+    C, p, q, *_ = ora.gaussian_problem(m, n, 23 + m)
+    pr = ora.Problem(C.astype(np.float32).astype(np.float64), p, q)
+    alpha = param * (m + n)
+    oreg = oracle_reg(ora, kind, alpha, None, n)
+    st = ora.make_state(pr)
+    eng = otdr.Engine(m, n, "f32")
+    eng.set_problem(C, p, q)
+    eng.set_regularizer(dev_reg(kind, alpha, None, n))
+    eng.set_state()
+    assert eng.solve_path() == "stream"
+    assert eng.kernel_name().startswith("tstream_kernel" if kernel == "tma" else "stream_kernel")
+    rho = ora.default_stepsize(m, n)
+    done = 0
+    for k in (1, 9, 60):
+        for _ in range(k - done):
+            ora.step(st, pr, oreg, rho)
+        eng.step(rho, k - done)
+        done = k
+        g = eng.get_state()
+        assert g.k == st.k == k
+        for nm in ("X", "phi", "psi", "a", "b"):
+            assert rel(getattr(g, nm), getattr(st, nm)) <= 1e-5, (k, nm)
+    o = ora.solve(pr, oreg, tol_primal=1e-6, max_iter=5000)
+    eng.set_state()
+    rep = eng.solve(otdr.SolverOptions(tol_primal=1e-6, max_iter=5000, storage="f32"), with_state=False)
+    assert rep.termination.name == o.termination
+    assert abs(rep.iterations - o.iterations) <= 2
+    assert abs(rep.objective - o.objective) <= 1e-6 * max(abs(o.objective), 1e-300)
+    eng.close()
