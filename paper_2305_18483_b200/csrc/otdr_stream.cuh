@@ -75,6 +75,18 @@ struct StreamArgs {
   int rank, nranks;
 };
 
+// Stripe-completion counter: gpu-scope acq_rel atomic by one thread after a
+// CTA barrier. The release half is cumulative over the CTA's stores that
+// bar.sync ordered before it (the colpart partials of the tile), the acquire
+// half over every other CTA's released partials -- so no per-thread
+// __threadfence (a full fence plus an L1 invalidate) is needed on either
+// side; the folding CTA reads the partials with ld.global.cg (L2).
+__device__ __forceinline__ unsigned atomic_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 // ---- peer-memory exchange helpers (system scope)
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -371,15 +383,13 @@ __device__ __forceinline__ void stream_segment_async(const StreamArgs& A, int ti
 // s_j^2 (column folds leave the critical path except for the last stripes).
 __device__ __forceinline__ void stream_stripe_done(const StreamArgs& A, long long stripe,
                                                    double* sred, bool* s_last, int par) {
-  __threadfence();  // this thread's colpart stores
-  __syncthreads();
+  __syncthreads();  // the CTA's colpart stores before thread 0's release
   if (threadIdx.x == 0) {
     const unsigned need = (unsigned)(A.sfirst[stripe + 1] - A.sfirst[stripe]);
-    *s_last = atomicAdd(A.scnt + stripe, 1u) == need - 1;
+    *s_last = atomic_add_acq_rel_gpu(A.scnt + stripe, 1u) == need - 1;
   }
-  __syncthreads();
+  __syncthreads();  // thread 0's acquire before every thread's ld.cg of the partials
   if (!*s_last) return;
-  __threadfence();
   const long long j = stripe * kStreamTN + threadIdx.x;
   double ss = 0.0;
   if (threadIdx.x < kStreamTN && j < A.n) {

@@ -95,15 +95,13 @@ __device__ __forceinline__ void ts_flush(const StreamArgs& A, int tile, long lon
     for (int w = 0; w < NCW; ++w) sum += red[w * kStreamTN + threadIdx.x];
     st_hint(A.colpart + (long long)tile * kStreamTN + threadIdx.x, sum, plast);
   }
-  __threadfence();  // this thread's colpart store
-  named_bar_sync(1, NC);
+  named_bar_sync(1, NC);  // the consumers' colpart stores before thread 0's release
   if (threadIdx.x == 0) {
     const unsigned need = (unsigned)(A.sfirst[stripe + 1] - A.sfirst[stripe]);
-    *s_last = atomicAdd(A.scnt + stripe, 1u) == need - 1;
+    *s_last = atomic_add_acq_rel_gpu(A.scnt + stripe, 1u) == need - 1;  // otdr_stream.cuh
   }
-  named_bar_sync(1, NC);
+  named_bar_sync(1, NC);  // thread 0's acquire before the ld.cg of the partials
   if (!*s_last) return;
-  __threadfence();
   const long long j = stripe * kStreamTN + threadIdx.x;
   double ss = 0.0;
   if (threadIdx.x < kStreamTN && j < A.n) {
