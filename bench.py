@@ -498,7 +498,9 @@ def run_ours(args):
         roof["traffic_source"] = "in-run (NVML GPM)"
     roof["dram_inrun"] = dram
 
-    # time to tolerance (device-resident solve loop)
+    # time to tolerance (device-resident solve loop) from make_state: the
+    # timed steps above advanced the state, so re-seed it first
+    eng.set_state()
     t_rep = eng.solve(otdr.SolverOptions(tol_primal=1e-4, max_iter=5000, storage="f32"),
                       with_state=False)
     tt = max_over_ranks(dist, t_rep.device_ms)

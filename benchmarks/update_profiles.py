@@ -43,15 +43,36 @@ def l2_compression(rep):
     return got
 
 
+def sass_tma(kernel):
+    """Counts of Blackwell async-copy SASS (UTMALDG = 2-D TMA loads, UBLKCP =
+    1-D bulk copies) and of LDGSTS (per-thread cp.async) in the kernel's code."""
+    so = os.path.join(ROOT, "paper_2305_18483_b200", "libotdr_dev.so")
+    try:
+        out = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
+    except Exception:
+        return None
+    name = kernel.split("<")[0].split("(")[0].split()[-1]
+    counts, cur = {}, None
+    for ln in out.splitlines():
+        if "Function :" in ln:
+            cur = ln
+        elif cur and name in cur:
+            for op in ("UTMALDG", "UBLKCP", "LDGSTS", "SYNCS"):
+                if op in ln:
+                    counts[op] = counts.get(op, 0) + 1
+    return counts
+
+
 def main():
     tag = sys.argv[1]
     if os.path.exists(os.path.join(OUT, "stream.ncu-rep")):
         s = summ(os.path.join(OUT, "stream.ncu-rep"))
-        it = 2
+        it = 20  # capture_profiles.sh: the timed launch of bench.py --steps 20 --warmup 5
         raw(os.path.join(OUT, "stream.ncu-rep"), os.path.join(PROF, f"{tag}_stream_20000_f32_raw.csv"))
         json.dump({"workload": W, "kernel": s["kernel"],
                    "source": f"profiles/{tag}_stream_20000_f32_raw.csv (ncu --set full --clock-control none; "
-                             "the timed launch of bench.py --steps 2 = ONE launch running 2 DR iterations)",
+                             "the timed launch of bench.py --steps 20 --warmup 5 = ONE launch running "
+                             "iterations 6..25)",
                    "iterations_in_launch": it, "dram_bytes_read": s["dram_read"],
                    "dram_bytes_write": s["dram_write"], "dram_bytes_per_launch": s["dram_bytes"],
                    "dram_bytes_per_iteration": s["dram_bytes"] / it,
@@ -60,6 +81,7 @@ def main():
                    "dram_throughput_pct_of_ncu_peak": s["dram_throughput_pct"], "registers": s["registers"],
                    "grid": s["grid"], "stalls": s.get("stalls"), "issue_active_pct": s.get("issue_active_pct"),
                    "x_allocation": "generic-compressible HBM (first 3.2 GB of X; OTDR_COMPRESS)",
+                   "sass_tma": sass_tma(s["kernel"]),
                    "l2_compression": l2_compression(os.path.join(OUT, "stream.ncu-rep"))},
                   open(os.path.join(PROF, "ncu_stream_summary.json"), "w"), indent=1)
     if os.path.exists(os.path.join(OUT, "sweep.ncu-rep")):
