@@ -29,8 +29,15 @@ src, tgt = datagen.gaussian_points(m, n, 1)
 p, q = datagen.uniform(m), datagen.uniform(n)
 
 
+# --no-conditional: racecheck aborts on CUDA graphs with conditional (WHILE)
+# nodes, which solve() uses on the graph loop (traces, OTDR_STREAM=off); with
+# this flag those cases run step() (plain chunk graphs) instead.
+NO_COND = "--no-conditional" in sys.argv
+
+
 def run(storage, reg, env=None, fused=False, trace=False):
     env = env or {}
+    graph_loop = trace or env.get("OTDR_STREAM") == "off"
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
@@ -38,6 +45,21 @@ def run(storage, reg, env=None, fused=False, trace=False):
         eng.build_sqdist_cost(src, tgt, p, q)
         eng.set_regularizer(reg)
         eng.set_state()
+        if NO_COND and graph_loop:
+            os.environ["OTDR_STREAM"] = "off"
+            eng.close()
+            eng = otdr.Engine(m, n, storage)
+            eng.build_sqdist_cost(src, tgt, p, q)
+            eng.set_regularizer(reg)
+            eng.set_state()
+            eng.step(otdr.default_stepsize(m, n), 40)
+            print(storage, reg.name(), env, "graph loop via step()", eng.kernel_name(),
+                  eng.get_state(with_plan=False).k, flush=True)
+            os.environ.pop("OTDR_STREAM")
+            if "OTDR_STREAM" in env:
+                os.environ["OTDR_STREAM"] = env["OTDR_STREAM"]
+            eng.close()
+            return
         r = eng.solve(otdr.SolverOptions(tol_primal=1e-5, max_iter=40, fused=fused, storage=storage,
                                          record_trace=trace, check_every=10 if trace else 1),
                       with_state=False)
@@ -72,11 +94,14 @@ if "--peer" in sys.argv:
         e = otdr.Engine(m, n, "f32", shard=otdr.Shard(rank, 2, lo, hi, None))
         engs.append(e)
     otdr.link_local(engs)
-    for e in engs:
+
+    def rank_run(e):  # the cost max, make_state sums and the steps are collective
         e.build_sqdist_cost(src[e.row_begin:e.row_end], tgt, p[e.row_begin:e.row_end], q)
         e.set_regularizer(quad)
         e.set_state()
-    ths = [threading.Thread(target=lambda e=e: e.step(otdr.default_stepsize(m, n), 20)) for e in engs]
+        e.step(otdr.default_stepsize(m, n), 20)
+
+    ths = [threading.Thread(target=rank_run, args=(e,)) for e in engs]
     for t in ths:
         t.start()
     for t in ths:
