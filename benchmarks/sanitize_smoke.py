@@ -89,15 +89,17 @@ run("f32", quad, {"OTDR_STREAM": "off"})
 # row-sharded: 2 rank contexts on this GPU, in-kernel peer exchange
 if "--peer" in sys.argv:
     os.environ["OTDR_STREAM_GRID"] = "64"
+    C = datagen.squared_distance_cost(src, tgt)
+    C /= C.max()
     engs = []
     for rank, (lo, hi) in enumerate(((0, 150), (150, 300))):
         e = otdr.Engine(m, n, "f32", shard=otdr.Shard(rank, 2, lo, hi, None))
+        e.set_problem(C[lo:hi], p[lo:hi], q)  # setup (allocations) before linking, like the tests
+        e.set_regularizer(quad)
         engs.append(e)
     otdr.link_local(engs)
 
-    def rank_run(e):  # the cost max, make_state sums and the steps are collective
-        e.build_sqdist_cost(src[e.row_begin:e.row_end], tgt, p[e.row_begin:e.row_end], q)
-        e.set_regularizer(quad)
+    def rank_run(e):  # make_state sums and the steps are collective: one thread per rank
         e.set_state()
         e.step(otdr.default_stepsize(m, n), 20)
 

@@ -286,6 +286,9 @@ struct otdr_dev {
   size_t str_part_cap = 0;
   double *str_part = nullptr, *str_colpart = nullptr;
   int str_big = 1, str_small = 1, str_head = 0;
+  int4* d_tiles = nullptr;     // streaming tiles {stripe, r0, r1, 0}, stripe-major
+  int str_fin_first = 1 << 30;  // first stripe of the final wave (folded in phase B)
+  bool str_fin = true;          // OTDR_STREAM_FIN=0: no final wave
   // streaming kernel: 1 = TMA producer warp + consumer warps (tstream_kernel,
   // the fp32-storage default), 0 = per-thread cp.async queues (stream_kernel;
   // fp64 storage, and fp32 with OTDR_STREAM_KERNEL=async); ts_cfg picks the
@@ -773,29 +776,39 @@ struct otdr_dev {
     const long long small = std::min(big, std::max<long long>(std::min<long long>(96, min_rows), big / std::max(1, str_tail)));
     const long long tail_stripes =
         str_tail > 1 ? std::min<long long>(S, (P * big + m_loc - 1) / m_loc) : 0;
-    std::vector<int> first;
-    long long ntiles = 0;
-    for (long long st = 0; st < S; ++st) {
-      first.push_back(int(ntiles));
-      const long long R = st >= S - tail_stripes ? small : big;
-      ntiles += (m_loc + R - 1) / R;
-    }
-    first.push_back(int(ntiles));
     // TMA kernel: tiles are whole blocks of ts_rb() rows (a block never
     // straddles two tiles, and phi block copies stay 16-byte aligned)
     const long long rb = use_tstream() ? ts_rb() : 1;
-    str_big = int((big + rb - 1) / rb * rb);
-    str_small = int((small + rb - 1) / rb * rb);
-    if (rb > 1) {
-      first.clear();
-      ntiles = 0;
-      for (long long st = 0; st < S; ++st) {
-        first.push_back(int(ntiles));
-        const long long R = st >= S - tail_stripes ? str_small : str_big;
-        ntiles += (m_loc + R - 1) / R;
-      }
-      first.push_back(int(ntiles));
+    auto rnd = [&](long long v) { return (v + rb - 1) / rb * rb; };
+    str_big = int(rnd(big));
+    str_small = int(rnd(small));
+    // Final wave: the last fin stripes are cut into short tiles (about one
+    // tile per CTA in all), so the sweep ends on ~fin-row tiles instead of a
+    // 96..128-row one (the one-tile finish spread of the sweep); their column
+    // folds move from the completing CTA to phase B, one stripe per CTA in
+    // parallel (a stripe of many short tiles would otherwise put a long fold
+    // on the critical path). OTDR_STREAM_FIN=0 disables it.
+    long long fin_rows = std::max<long long>(32, rnd((m_loc + P - 1) / P));
+    long long fin = 0;
+    if (str_fin && S > 1) {
+      const long long per = (m_loc + fin_rows - 1) / fin_rows;
+      fin = std::min<long long>({(P + per - 1) / per, S - 1, P});
     }
+    fin_rows = rnd(fin_rows);
+    std::vector<int> first;
+    std::vector<int4> tiles;
+    for (long long st = 0; st < S; ++st) {
+      first.push_back(int(tiles.size()));
+      const long long R = st >= S - fin ? fin_rows : st >= S - tail_stripes ? str_small : str_big;
+      for (long long r0 = 0; r0 < m_loc; r0 += R)
+        tiles.push_back(int4{int(st), int(r0), int(std::min(m_loc, r0 + R)), 0});
+    }
+    first.push_back(int(tiles.size()));
+    const long long ntiles = (long long)tiles.size();
+    str_fin_first = int(S - fin);
+    if (d_tiles) cudaFree(d_tiles);
+    d_tiles = dalloc<int4>(tiles.size());
+    CK(cudaMemcpy(d_tiles, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
     str_head = int(S - tail_stripes);
     for (void* ptr : {(void*)str_part, (void*)str_colpart, (void*)d_sfirst,
                       (void*)d_scnt, (void*)str_sspart})
@@ -912,6 +925,8 @@ struct otdr_dev {
                          d_sfirst, d_scnt, str_sspart, str_part, d_ctl, d_prm, m_loc, n, ld, int(S), str_ntiles,
                          iters, nullptr, m_glob, sharded ? d_peers : nullptr, rbuf, d_xep,
                          cfg.rank, cfg.nranks};
+    sa.tiles = d_tiles;
+    sa.fin_first = str_fin_first;
     static const bool trace = std::getenv("OTDR_STREAM_TRACE") != nullptr;
     unsigned long long* ts = nullptr;
     const size_t tsn = size_t(otdrk::kTraceIters) * size_t(str_P + 12);
@@ -1340,6 +1355,7 @@ struct otdr_dev {
       comp_free(C, c_vmm);
       C = nullptr;
     }
+    if (d_tiles) cudaFree(d_tiles);
     void* ptrs[] = {C, X, p, q, phi, psi, a, b, r, s, rowpart, colpart, exch, bpart, cpart,
                     str_part, str_colpart, d_sfirst, d_scnt, str_sspart, d_glp_pos,
                     csum, stage, gscratch, d_dev_row, d_seg, d_cert_seg, d_prm, d_ctl, d_trace, d_mx};
@@ -1586,6 +1602,7 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     if (const char* sd = std::getenv("OTDR_STREAM_D")) ctx->str_d = std::atoi(sd);
     if (const char* sk = std::getenv("OTDR_STREAM_KERNEL")) ctx->str_kind = std::strcmp(sk, "async") == 0 ? 0 : 1;
     if (const char* tc = std::getenv("OTDR_TS_CFG")) ctx->ts_cfg = std::atoi(tc);
+    if (const char* fe = std::getenv("OTDR_STREAM_FIN")) ctx->str_fin = std::strcmp(fe, "0") != 0;
     ctx->plan_geometry();
     ctx->bpart = dalloc<double>(size_t(ctx->RB + ctx->CB) * 3);
     ctx->csum = dalloc<double>(otdrk::kCertVals);

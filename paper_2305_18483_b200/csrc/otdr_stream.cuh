@@ -73,6 +73,10 @@ struct StreamArgs {
   double* rbuf;           // this rank's receive buffer (== peers[rank])
   unsigned long long* xep;  // exchange epoch (monotonic, identical on every rank)
   int rank, nranks;
+  // tile table {stripe, r0, r1, 0}, stripe-major; stripes >= fin_first are the
+  // final wave of short tiles, folded in phase B (one stripe per CTA)
+  const int4* tiles;
+  int fin_first;
 };
 
 // Stripe-completion counter: gpu-scope acq_rel atomic by one thread after a
@@ -383,6 +387,10 @@ __device__ __forceinline__ void stream_segment_async(const StreamArgs& A, int ti
 // s_j^2 (column folds leave the critical path except for the last stripes).
 __device__ __forceinline__ void stream_stripe_done(const StreamArgs& A, long long stripe,
                                                    double* sred, bool* s_last, int par) {
+  if (stripe >= A.fin_first) {  // final-wave stripe: folded in phase B
+    __syncthreads();            // (the partial staging is reused by the next tile)
+    return;
+  }
   __syncthreads();  // the CTA's colpart stores before thread 0's release
   if (threadIdx.x == 0) {
     const unsigned need = (unsigned)(A.sfirst[stripe + 1] - A.sfirst[stripe]);
@@ -425,6 +433,55 @@ __device__ __forceinline__ void stream_stripe_done(const StreamArgs& A, long lon
 }
 
 
+// Phase-B fold of one final-wave stripe by a whole CTA (NT >= 256 threads):
+// the same fold as stream_stripe_done (tile order), after the grid barrier
+// made every tile's column partials visible.
+template <int NT>
+__device__ __forceinline__ void stream_fin_fold(const StreamArgs& A, long long stripe, double* sred,
+                                                int par, double* scratch) {
+  // warp w sums tiles w, w + NW, ... of every column (independent loads in
+  // flight), then the NW partials are added in warp order: a fixed order.
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t0 = A.sfirst[stripe], t1 = A.sfirst[stripe + 1];
+  double acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+  for (int t = t0 + warp; t < t1; t += NW) {
+    const double* src = A.colpart + (long long)t * kStreamTN + lane;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] += __ldcg(src + 32 * e);
+  }
+  __syncthreads();  // scratch (NW x 256 doubles) free
+#pragma unroll
+  for (int e = 0; e < 8; ++e) scratch[warp * kStreamTN + 32 * e + lane] = acc[e];
+  __syncthreads();
+  const long long j = stripe * kStreamTN + threadIdx.x;
+  double ss = 0.0;
+  if (threadIdx.x < kStreamTN && j < A.n) {
+    double Ssum = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) Ssum += scratch[w * kStreamTN + threadIdx.x];
+    // scratch may be a TMA ring: order these generic accesses before the
+    // next iteration's async-proxy (TMA) writes into it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (A.peers) {
+      for (int r = 0; r < A.nranks; ++r) xslot(A.peers[r], par, A.rank, A.nranks, A.n)[j] = Ssum;
+    } else {
+      const double sj = __dsub_rn(Ssum, A.q[j]);
+      A.s[j] = sj;
+      ss = sj * sj;
+    }
+  }
+  if (A.peers) {
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+    return;
+  }
+  const double tot = block_sum_n<NT / 32>(ss, sred);
+  if (threadIdx.x == 0) A.sspart[stripe] = tot;
+}
+
 // Loop state of a persistent streaming solve (identical in every CTA).
 struct StreamLoop {
   long long k, last_imp, k0, it;
@@ -442,7 +499,8 @@ struct StreamLoop {
 template <int NT, typename Stamp>
 __device__ __forceinline__ bool stream_finish_iteration(const StreamArgs& A, const Params& prm,
                                                         StreamLoop& L, double* sred, double* bc,
-                                                        unsigned long long* bar, Stamp&& stamp) {
+                                                        unsigned long long* bar, Stamp&& stamp,
+                                                        double* scratch) {
   Ctl* ctl = A.ctl;
   const int c = (int)blockIdx.x, P = (int)gridDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -453,6 +511,8 @@ __device__ __forceinline__ bool stream_finish_iteration(const StreamArgs& A, con
   const long long k0 = L.k0;
   const bool peer = A.peers != nullptr;
     grid_barrier(bar);
+    if (c < A.stripes - A.fin_first)  // final-wave stripes, one per CTA
+      stream_fin_fold<NT>(A, A.fin_first + c, sred, int(L.epoch & 1), scratch);
     stamp(P + 1);
 
     // ---- B. row folds (warp per row, stripe order) and column folds (CTA order)
@@ -675,7 +735,6 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
   // fused even/odd path (solver.cpp:127-177): the X buffer alternates
   // between X (even iterations read C) and B = X - rho C (odd ones do not)
   L.shifted = prm.fused ? ctl->fused_shifted : 0;
-  const long long m = A.m;
 
   auto stamp = [&](int slot) {
     if (A.tstamp && L.it < kTraceIters && threadIdx.x == 0 && (slot < P ? true : c == 0))
@@ -690,26 +749,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
       __syncthreads();
       const int tile = (int)s_tile;  // the tile sweep ends with __syncthreads
       if (tile >= A.ntiles) break;
-      int4 tl;
-      {
-        const int hb = A.head * A.nb;
-        int st_, k_, R_;
-        if (tile < hb) {
-          st_ = tile / A.nb;
-          k_ = tile - st_ * A.nb;
-          R_ = A.big;
-        } else {
-          const int t2 = tile - hb;
-          const int q2 = t2 / A.ns;
-          st_ = A.head + q2;
-          k_ = t2 - q2 * A.ns;
-          R_ = A.small;
-        }
-        const long long r0_ = (long long)k_ * R_;
-        tl.x = st_;
-        tl.y = (int)r0_;
-        tl.z = (int)((r0_ + R_ < m) ? r0_ + R_ : m);
-      }
+      int4 tl = A.tiles[tile];  // {stripe, r0, r1}
       if constexpr (D > 0) {
         if (fmode == MODE_EVEN)
           stream_segment_async<T, REG, EXACT, NV, D, MODE_EVEN>(A, tile, tl.x, tl.y, tl.z, rho, qd, qinv, red, squeue);
@@ -723,7 +763,8 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(StreamArgs A) {
       stream_stripe_done(A, tl.x, sred, &s_last, int(L.epoch & 1));
     }
     stamp(c);
-    if (stream_finish_iteration<kThreads>(A, prm, L, sred, bc, &ctl->bar_str, stamp)) break;
+    // scratch for the final-wave folds: the (drained) cp.async queue / staging
+    if (stream_finish_iteration<kThreads>(A, prm, L, sred, bc, &ctl->bar_str, stamp, &red[0][0])) break;
   }
 }
 

@@ -95,6 +95,10 @@ __device__ __forceinline__ void ts_flush(const StreamArgs& A, int tile, long lon
     for (int w = 0; w < NCW; ++w) sum += red[w * kStreamTN + threadIdx.x];
     st_hint(A.colpart + (long long)tile * kStreamTN + threadIdx.x, sum, plast);
   }
+  if (stripe >= A.fin_first) {  // final-wave stripe: folded in phase B
+    named_bar_sync(1, NC);       // red is reused by the next tile
+    return;
+  }
   named_bar_sync(1, NC);  // the consumers' colpart stores before thread 0's release
   if (threadIdx.x == 0) {
     const unsigned need = (unsigned)(A.sfirst[stripe + 1] - A.sfirst[stripe]);
@@ -295,7 +299,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
   L.it = 0;
   L.epoch = (A.peers != nullptr ? *A.xep : 0ull) + 1;
   L.shifted = prm.fused ? ctl->fused_shifted : 0;
-  const long long m = A.m;
   // ring position: the same sequence in the producer and the consumers
   int ring = 0;
   unsigned round = 0;
@@ -327,21 +330,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
             }
             break;
           }
-          int st_, k_, R_;
-          const int hb = A.head * A.nb;
-          if (tile < hb) {
-            st_ = tile / A.nb;
-            k_ = tile - st_ * A.nb;
-            R_ = A.big;
-          } else {
-            const int t2 = tile - hb;
-            const int q2 = t2 / A.ns;
-            st_ = A.head + q2;
-            k_ = t2 - q2 * A.ns;
-            R_ = A.small;
-          }
-          const long long r0 = (long long)k_ * R_;
-          const long long r1 = (r0 + R_ < m) ? r0 + R_ : m;
+          const int4 tl = A.tiles[tile];  // {stripe, r0, r1}
+          const int st_ = tl.x;
+          const long long r0 = tl.y, r1 = tl.z;
           const int col0 = st_ * kStreamTN;
           for (long long rb = r0; rb < r1; rb += RB) {
             mbar_wait(&empty[ring], round ^ 1u);
@@ -383,7 +374,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
       fence_proxy_async_global();
     }
     stamp(c);
-    if (stream_finish_iteration<NT>(A, prm, L, sred, bc, &ctl->bar_tst, stamp)) break;
+    // scratch for the final-wave folds: the ring (idle between sweeps)
+    if (stream_finish_iteration<NT>(A, prm, L, sred, bc, &ctl->bar_tst, stamp,
+                                    reinterpret_cast<double*>(ts_smem + LY::oTiles)))
+      break;
   }
 }
 
