@@ -206,17 +206,25 @@ inline void* comp_malloc(int device, size_t bytes, size_t comp_bytes, size_t* si
   if (d.reserve(&va, size, g, 0, 0) != CUDA_SUCCESS) return nullptr;
   size_t mapped = 0;
   bool fail = false;
+  // OTDR_COMPRESS_CHUNK_MB: physical allocations of at most this size
+  // (0 = one allocation per part)
+  size_t chunk = 0;
+  if (const char* cm = std::getenv("OTDR_COMPRESS_CHUNK_MB")) chunk = size_t(std::atoll(cm)) << 20;
+  if (chunk) chunk = std::max(g, chunk / g * g);
   for (int part = 0; part < 2 && !fail; ++part) {
-    const size_t len = part == 0 ? csize : size - csize;
-    if (!len) continue;
-    CUmemGenericAllocationHandle h;
-    if (d.create(&h, len, part == 0 ? &prop : &plain, 0) != CUDA_SUCCESS) {
-      fail = true;
-      break;
+    size_t len = part == 0 ? csize : size - csize;
+    while (len && !fail) {
+      const size_t piece = chunk ? std::min(chunk, len) : len;
+      CUmemGenericAllocationHandle h;
+      if (d.create(&h, piece, part == 0 ? &prop : &plain, 0) != CUDA_SUCCESS) {
+        fail = true;
+        break;
+      }
+      if (d.map(va + mapped, piece, 0, h, 0) != CUDA_SUCCESS) fail = true;
+      else mapped += piece;
+      d.release(h);  // the mapping keeps the physical memory alive
+      len -= piece;
     }
-    if (d.map(va + mapped, len, 0, h, 0) != CUDA_SUCCESS) fail = true;
-    else mapped += len;
-    d.release(h);  // the mapping keeps the physical memory alive
   }
   CUmemAccessDesc acc{};
   acc.location = prop.location;
@@ -288,7 +296,7 @@ struct otdr_dev {
   int str_big = 1, str_small = 1, str_head = 0;
   int4* d_tiles = nullptr;     // streaming tiles {stripe, r0, r1, 0}, stripe-major
   int str_fin_first = 1 << 30;  // first stripe of the final wave (folded in phase B)
-  bool str_fin = true;          // OTDR_STREAM_FIN=0: no final wave
+  bool str_fin = false;         // OTDR_STREAM_FIN=1: final wave (measured slower)
   // streaming kernel: 1 = TMA producer warp + consumer warps (tstream_kernel,
   // the fp32-storage default), 0 = per-thread cp.async queues (stream_kernel;
   // fp64 storage, and fp32 with OTDR_STREAM_KERNEL=async); ts_cfg picks the
@@ -787,7 +795,8 @@ struct otdr_dev {
     // 96..128-row one (the one-tile finish spread of the sweep); their column
     // folds move from the completing CTA to phase B, one stripe per CTA in
     // parallel (a stripe of many short tiles would otherwise put a long fold
-    // on the critical path). OTDR_STREAM_FIN=0 disables it.
+    // on the critical path). Off by default: at the 2500-row band the fold
+    // costs more than the narrower tail saves (OTDR_STREAM_FIN=1 enables it).
     long long fin_rows = std::max<long long>(32, rnd((m_loc + P - 1) / P));
     long long fin = 0;
     if (str_fin && S > 1) {
@@ -1602,7 +1611,7 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     if (const char* sd = std::getenv("OTDR_STREAM_D")) ctx->str_d = std::atoi(sd);
     if (const char* sk = std::getenv("OTDR_STREAM_KERNEL")) ctx->str_kind = std::strcmp(sk, "async") == 0 ? 0 : 1;
     if (const char* tc = std::getenv("OTDR_TS_CFG")) ctx->ts_cfg = std::atoi(tc);
-    if (const char* fe = std::getenv("OTDR_STREAM_FIN")) ctx->str_fin = std::strcmp(fe, "0") != 0;
+    if (const char* fe = std::getenv("OTDR_STREAM_FIN")) ctx->str_fin = std::strcmp(fe, "1") == 0;
     ctx->plan_geometry();
     ctx->bpart = dalloc<double>(size_t(ctx->RB + ctx->CB) * 3);
     ctx->csum = dalloc<double>(otdrk::kCertVals);
