@@ -206,27 +206,18 @@ inline void* comp_malloc(int device, size_t bytes, size_t comp_bytes, size_t* si
   if (d.reserve(&va, size, g, 0, 0) != CUDA_SUCCESS) return nullptr;
   size_t mapped = 0;
   bool fail = false;
-  // OTDR_COMPRESS_CHUNK_MB: physical allocations of at most this size
-  // (0 = one allocation per part)
-  size_t chunk = 0;
-  if (const char* cm = std::getenv("OTDR_COMPRESS_CHUNK_MB")) chunk = size_t(std::atoll(cm)) << 20;
-  if (chunk) chunk = std::max(g, chunk / g * g);
   for (int part = 0; part < 2 && !fail; ++part) {
-    size_t len = part == 0 ? csize : size - csize;
-    while (len && !fail) {
-      const size_t piece = chunk ? std::min(chunk, len) : len;
-      CUmemGenericAllocationHandle h;
-      if (d.create(&h, piece, part == 0 ? &prop : &plain, 0) != CUDA_SUCCESS) {
-        fail = true;
-        break;
-      }
-      if (d.map(va + mapped, piece, 0, h, 0) != CUDA_SUCCESS) fail = true;
-      else mapped += piece;
-      d.release(h);  // the mapping keeps the physical memory alive
-      len -= piece;
+    const size_t len = part == 0 ? csize : size - csize;
+    if (!len) continue;
+    CUmemGenericAllocationHandle h;
+    if (d.create(&h, len, part == 0 ? &prop : &plain, 0) != CUDA_SUCCESS) {
+      fail = true;
+      break;
     }
-  }
-  CUmemAccessDesc acc{};
+    if (d.map(va + mapped, len, 0, h, 0) != CUDA_SUCCESS) fail = true;
+    else mapped += len;
+    d.release(h);  // the mapping keeps the physical memory alive
+  }  CUmemAccessDesc acc{};
   acc.location = prop.location;
   acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
   if (fail || d.access(va, size, &acc, 1) != CUDA_SUCCESS) {
