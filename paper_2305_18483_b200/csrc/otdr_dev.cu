@@ -284,7 +284,7 @@ struct otdr_dev {
   int str_P = 0, str_ntiles = 0, str_tpc = 0, str_tail = 4;
   size_t str_part_cap = 0;
   double *str_part = nullptr, *str_colpart = nullptr;
-  int str_big = 1, str_small = 1, str_head = 0;
+  int str_big = 1, str_small = 1;  // streaming tile rows (long / tail tiles)
   int4* d_tiles = nullptr;     // streaming tiles {stripe, r0, r1, 0}, stripe-major
   int str_fin_first = 1 << 30;  // first stripe of the final wave (folded in phase B)
   bool str_fin = false;         // OTDR_STREAM_FIN=1: final wave (measured slower)
@@ -809,7 +809,6 @@ struct otdr_dev {
     if (d_tiles) cudaFree(d_tiles);
     d_tiles = dalloc<int4>(tiles.size());
     CK(cudaMemcpy(d_tiles, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    str_head = int(S - tail_stripes);
     for (void* ptr : {(void*)str_part, (void*)str_colpart, (void*)d_sfirst,
                       (void*)d_scnt, (void*)str_sspart})
       if (ptr) cudaFree(ptr);
@@ -919,9 +918,7 @@ struct otdr_dev {
 
   void launch_stream(long long iters) {
     const long long S = (ld + otdrk::kStreamTN - 1) / otdrk::kStreamTN;
-    const int nb = int((m_loc + str_big - 1) / str_big), ns = int((m_loc + str_small - 1) / str_small);
     otdrk::StreamArgs sa{X, C, phi, a, r, p, psi, b, s, q, rowpart, str_colpart,
-                         str_big, str_small, str_head, nb, ns,
                          d_sfirst, d_scnt, str_sspart, str_part, d_ctl, d_prm, m_loc, n, ld, int(S), str_ntiles,
                          iters, nullptr, m_glob, sharded ? d_peers : nullptr, rbuf, d_xep,
                          cfg.rank, cfg.nranks};

@@ -52,10 +52,7 @@ struct StreamArgs {
   const double* q;
   double* rowpart;        // [m][stripes]
   double* colpart;        // [ntiles][TN] one slot per tile
-  // tiles, stripe-major: the first `head` stripes in row runs of `big`, the
-  // rest in runs of `small` (tile id -> stripe / rows is arithmetic, no load)
-  int big, small, head, nb, ns;
-  const int* sfirst;      // [stripes + 1] first tile of each stripe
+  const int* sfirst;      // [stripes + 1] first tile of each stripe (tiles: see `tiles`)
   unsigned* scnt;         // [stripes] tiles completed this sweep (zero between sweeps)
   double* sspart;         // [stripes] sum of s_j^2 over the stripe's columns
   double* part;           // [P][4]
