@@ -871,10 +871,9 @@ struct otdr_dev {
   }
 
   // ---- TMA-producer streaming kernel (otdr_tstream.cuh)
-  // geometry (consumer warps, rows per block, ring stages): fp32 8/16/5,
-  // fp64 8/8/5 (~187 KB of shared memory, one CTA per SM); OTDR_TS_CFG=1
-  // selects 16 consumer warps
-  int ts_rb() const { return ts_cfg == 1 ? 16 : 8; }
+  // geometry (consumer warps, rows per block, ring stages, CTAs per SM):
+  // 4/8/3/3 by default; OTDR_TS_CFG=1: 8/8/5/2, 2: 16/16/5/1
+  int ts_rb() const { return ts_cfg == 2 ? 16 : 8; }
   template <typename T, int REG, int NCW, int RB, int S, int MINB>
   void tstream_call(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
     constexpr bool E = sizeof(T) == 8;
@@ -897,11 +896,15 @@ struct otdr_dev {
   }
   template <typename T, int REG>
   void tstream_dispatch_t(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
-    // fp32: two CTAs per SM of 8 consumer warps (one row per warp per block)
-    // + a producer warp, 5-stage ring of 8-row blocks (~106 KB per CTA);
-    // OTDR_TS_CFG=1: one CTA of 16 consumer warps, 16-row blocks
-    if (ts_cfg == 1) tstream_call<T, REG, 16, 16, 5, 1>(lc, sa, occ);
-    else tstream_call<T, REG, 8, 8, 5, 2>(lc, sa, occ);
+    // fp32: three CTAs per SM of 4 consumer warps (two rows per warp per
+    // block) + a producer warp, 3-stage ring of 8-row blocks (~63 KB per CTA);
+    // OTDR_TS_CFG=1: the round-2 geometry (two CTAs of 8 consumer warps, one
+    // row each, 5 stages), 2: one CTA of 16 consumer warps, 16-row blocks
+    //
+    if (ts_cfg == 1) tstream_call<T, REG, 8, 8, 5, 2>(lc, sa, occ);
+    else if (ts_cfg == 2) tstream_call<T, REG, 16, 16, 5, 1>(lc, sa, occ);
+    else if (ts_cfg == 3) tstream_call<T, REG, 4, 8, 2, 4>(lc, sa, occ);
+    else tstream_call<T, REG, 4, 8, 3, 3>(lc, sa, occ);
   }
   void tstream_dispatch(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
     const bool quad = reg_kind == OTDR_REG_QUAD;

@@ -89,11 +89,11 @@ __device__ __forceinline__ void ts_flush(const StreamArgs& A, int tile, long lon
 #pragma unroll
     for (int e = 0; e < VEC; ++e) red[warp * kStreamTN + v * 32 * VEC + lane * VEC + e] = cacc[v][e];
   named_bar_sync(1, NC);
-  if (threadIdx.x < kStreamTN) {
+  for (int col = threadIdx.x; col < kStreamTN; col += NC) {
     double sum = 0.0;
 #pragma unroll
-    for (int w = 0; w < NCW; ++w) sum += red[w * kStreamTN + threadIdx.x];
-    st_hint(A.colpart + (long long)tile * kStreamTN + threadIdx.x, sum, plast);
+    for (int w = 0; w < NCW; ++w) sum += red[w * kStreamTN + col];
+    st_hint(A.colpart + (long long)tile * kStreamTN + col, sum, plast);
   }
   if (stripe >= A.fin_first) {  // final-wave stripe: folded in phase B
     named_bar_sync(1, NC);       // red is reused by the next tile
@@ -106,10 +106,11 @@ __device__ __forceinline__ void ts_flush(const StreamArgs& A, int tile, long lon
   }
   named_bar_sync(1, NC);  // thread 0's acquire before the ld.cg of the partials
   if (!*s_last) return;
-  const long long j = stripe * kStreamTN + threadIdx.x;
   double ss = 0.0;
-  if (threadIdx.x < kStreamTN && j < A.n) {
-    const double* src = A.colpart + threadIdx.x;
+  for (int col = threadIdx.x; col < kStreamTN; col += NC) {  // NC may be < kStreamTN
+    const long long j = stripe * kStreamTN + col;
+    if (j >= A.n) break;
+    const double* src = A.colpart + col;
     const int t0 = A.sfirst[stripe], t1 = A.sfirst[stripe + 1];
     double Ssum = 0.0;
 #pragma unroll 16
@@ -119,7 +120,7 @@ __device__ __forceinline__ void ts_flush(const StreamArgs& A, int tile, long lon
     } else {
       const double sj = __dsub_rn(Ssum, A.q[j]);
       A.s[j] = sj;
-      ss = sj * sj;
+      ss += sj * sj;
     }
   }
   if (A.peers) {
@@ -243,12 +244,24 @@ __device__ __forceinline__ void ts_consume(const StreamArgs& A, unsigned char* s
       ring = 0;
       round ^= 1u;
     }
+    if constexpr (RPW == 2) {
+      // both rows at once: one exchange halves the pair (lanes 0-15 keep row
+      // u = 0, lanes 16-31 row u = 1), then a 16-lane butterfly
+      const bool hi = lane & 16;
+      double tot = (hi ? rs[1] : rs[0]) + __shfl_xor_sync(0xffffffffu, hi ? rs[0] : rs[1], 16);
 #pragma unroll
-    for (int u = 0; u < RPW; ++u) {
-      const int t = warp + u * NCW;
-      if (t < md.nrows) {
-        const double tot = warp_sum(rs[u]);
-        if (lane == 0) st_hint(A.rowpart + (long long)(md.row0 + t) * A.stripes + stripe, tot, plast);
+      for (int o = 8; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      const int t = warp + (hi ? NCW : 0);
+      if ((lane & 15) == 0 && t < md.nrows)
+        st_hint(A.rowpart + (long long)(md.row0 + t) * A.stripes + stripe, tot, plast);
+    } else {
+#pragma unroll
+      for (int u = 0; u < RPW; ++u) {
+        const int t = warp + u * NCW;
+        if (t < md.nrows) {
+          const double tot = warp_sum(rs[u]);
+          if (lane == 0) st_hint(A.rowpart + (long long)(md.row0 + t) * A.stripes + stripe, tot, plast);
+        }
       }
     }
     if (md.flags & kTSLast) ts_flush<NCW, NV, VEC>(A, md.tile, stripe, cacc, red, sred, s_last, par, plast);
@@ -264,7 +277,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
                    const __grid_constant__ CUtensorMap mapC) {
   using LY = TSLayout<T, NCW, RB, S>;
   constexpr int NT = (NCW + 1) * 32;
-  static_assert(RB % NCW == 0 && NCW * 32 >= kStreamTN, "consumer geometry");
+  static_assert(RB % NCW == 0 && RB % 2 == 0, "consumer geometry");
   Ctl* ctl = A.ctl;
   if (ctl->done) return;  // grid-uniform
   const Params& prm = *A.prm;
