@@ -903,7 +903,6 @@ struct otdr_dev {
     //
     if (ts_cfg == 1) tstream_call<T, REG, 8, 8, 5, 2>(lc, sa, occ);
     else if (ts_cfg == 2) tstream_call<T, REG, 16, 16, 5, 1>(lc, sa, occ);
-    else if (ts_cfg == 3) tstream_call<T, REG, 4, 8, 2, 4>(lc, sa, occ);
     else tstream_call<T, REG, 4, 8, 3, 3>(lc, sa, occ);
   }
   void tstream_dispatch(cudaLaunchConfig_t& lc, const otdrk::StreamArgs& sa, int* occ) {
