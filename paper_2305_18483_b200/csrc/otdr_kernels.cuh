@@ -546,15 +546,19 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned
                "r"(bytes)
                : "memory");
 }
+// try_wait's suspend-time hint: a waiting warp sleeps until the phase
+// completes (or the hint elapses) instead of re-issuing the probe -- spinning
+// consumers otherwise take issue slots from the warps that compute
+constexpr unsigned kMbarSuspendNs = 0x989680;
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_addr(bar)),
-      "r"(phase)
+      "r"(phase), "r"(kMbarSuspendNs)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
