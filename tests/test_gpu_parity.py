@@ -1109,3 +1109,43 @@ def test_fp32_stream_kernels_match_oracle(ora, monkeypatch, kernel, m, n, kind, 
     assert abs(rep.iterations - o.iterations) <= 2
     assert abs(rep.objective - o.objective) <= 1e-6 * max(abs(o.objective), 1e-300)
     eng.close()
+
+
+@pytest.mark.parametrize("ts_cfg", ["1", "2"])
+@pytest.mark.parametrize("m,n", [(5, 3000), (300, 517), (2100, 2501)])
+def test_tstream_geometries_match_oracle(ora, monkeypatch, ts_cfg, m, n):
+    """The non-default TMA-kernel geometries (OTDR_TS_CFG=1: 8 consumer warps
+    x 1 row, 5 stages, 2 CTAs/SM; 2: 16 warps, 16-row blocks) against the
+    oracle on the fp32-rounded cost, like the default geometry in
+    test_fp32_stream_kernels_match_oracle: iterates after k steps within 1e-5,
+    a full solve to the same termination, iterations within 2."""
+    monkeypatch.setenv("OTDR_RESIDENT", "off")
+    monkeypatch.setenv("OTDR_TS_CFG", ts_cfg)
+    C, p, q, *_ = ora.gaussian_problem(m, n, 41 + m)
+    pr = ora.Problem(C.astype(np.float32).astype(np.float64), p, q)
+    alpha = 0.7 * (m + n)
+    oreg = oracle_reg(ora, "quad", alpha, None, n)
+    st = ora.make_state(pr)
+    eng = otdr.Engine(m, n, "f32")
+    eng.set_problem(C, p, q)
+    eng.set_regularizer(dev_reg("quad", alpha, None, n))
+    eng.set_state()
+    assert eng.solve_path() == "stream"
+    assert eng.kernel_name().startswith("tstream_kernel")
+    rho = ora.default_stepsize(m, n)
+    done = 0
+    for k in (1, 20):
+        for _ in range(k - done):
+            ora.step(st, pr, oreg, rho)
+        eng.step(rho, k - done)
+        done = k
+        g = eng.get_state()
+        for nm in ("X", "phi", "psi", "a", "b"):
+            assert rel(getattr(g, nm), getattr(st, nm)) <= 1e-5, (k, nm)
+    o = ora.solve(pr, oreg, tol_primal=1e-6, max_iter=5000)
+    eng.set_state()
+    rep = eng.solve(otdr.SolverOptions(tol_primal=1e-6, max_iter=5000, storage="f32"), with_state=False)
+    assert rep.termination.name == o.termination
+    assert abs(rep.iterations - o.iterations) <= 2
+    assert abs(rep.objective - o.objective) <= 1e-6 * max(abs(o.objective), 1e-300)
+    eng.close()
