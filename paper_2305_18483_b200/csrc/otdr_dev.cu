@@ -272,6 +272,8 @@ struct otdr_dev {
   bool sharded = false;  // NCCL exchange path (row shards, or a 1-rank communicator)
   int res_G = 0, res_R = 0;
   size_t res_smem = 0;
+  // fp32 storage on fp64 shared-memory tiles when they fit (OTDR_RESIDENT_TILES=f32: storage type)
+  bool res_wide = false, res_allow_wide = true;
   double* gscratch = nullptr;
   // peer-memory exchange of row-sharded runs (CUDA IPC over NVLink)
   bool p2p = false;
@@ -732,8 +734,16 @@ struct otdr_dev {
     CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg.device));
     const long long G = std::min<long long>(num_sms, m_loc);
     const long long R = (m_loc + G - 1) / G;
-    const size_t bytes = f64() ? otdrk::resident_smem_bytes<double>(R, n, ld)
-                               : otdrk::resident_smem_bytes<float>(R, n, ld);
+    res_wide = false;
+    size_t bytes = f64() ? otdrk::resident_smem_bytes<double>(R, n, ld)
+                         : otdrk::resident_smem_bytes<float>(R, n, ld);
+    if (!f64() && res_allow_wide) {
+      const size_t wide = otdrk::resident_smem_bytes<double>(R, n, ld);
+      if (wide + 2048 <= size_t(max_smem)) {
+        bytes = wide;
+        res_wide = true;
+      }
+    }
     if (bytes + 2048 > size_t(max_smem)) return;
     res_G = int((m_loc + R - 1) / R);
     res_R = int(R);
@@ -1000,6 +1010,10 @@ struct otdr_dev {
     lc.numAttrs = 1;
     if (f64()) {
       auto kern = otdrk::resident_kernel<double, false>;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(res_smem)));
+      CK(cudaLaunchKernelEx(&lc, kern, ra));
+    } else if (res_wide) {
+      auto kern = otdrk::resident_kernel<double, false, float>;
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(res_smem)));
       CK(cudaLaunchKernelEx(&lc, kern, ra));
     } else {
@@ -1430,7 +1444,8 @@ const char* otdr_dev_kernel_name(const otdr_dev* ctx) {
   const char* st = c->f64() ? "f64" : "f32";
   const char* rg = c->reg_kind == OTDR_REG_QUAD ? "quad" : c->reg_kind == OTDR_REG_GROUP_LASSO ? "group-lasso" : "none";
   const int path = otdr_dev_solve_path(ctx);
-  if (path == OTDR_PATH_RESIDENT) c->kname = std::string("resident_kernel<") + st + ", " + rg + ">";
+  if (path == OTDR_PATH_RESIDENT)
+    c->kname = std::string("resident_kernel<") + st + (c->res_wide ? " storage, f64 tiles" : "") + ", " + rg + ">";
   else if (path == OTDR_PATH_STREAM && c->reg_kind == OTDR_REG_GROUP_LASSO)
     c->kname = std::string("gl_stream_kernel<") + st + ">";
   else if (path == OTDR_PATH_STREAM) {
@@ -1593,6 +1608,7 @@ otdr_status otdr_dev_create(const otdr_dev_config* cfg, otdr_dev** out) {
     ctx->exch = dalloc<double>(size_t(ctx->n) + 3);
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
     if (const char* re = std::getenv("OTDR_RESIDENT")) ctx->allow_resident = std::strcmp(re, "off") != 0;
+    if (const char* rt = std::getenv("OTDR_RESIDENT_TILES")) ctx->res_allow_wide = std::strcmp(rt, "f32") != 0;
     if (const char* st = std::getenv("OTDR_STREAM")) ctx->allow_stream = std::strcmp(st, "off") != 0;
     if (const char* gs = std::getenv("OTDR_GL_STREAM")) ctx->allow_gl_stream = std::strcmp(gs, "off") != 0;
     ctx->str_d = -1;

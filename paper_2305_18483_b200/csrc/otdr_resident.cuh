@@ -19,6 +19,8 @@
 #pragma once
 #include "otdr_kernels.cuh"
 
+#include <type_traits>
+
 namespace otdrk {
 
 constexpr int kRT = 512;       // threads per resident CTA
@@ -76,7 +78,11 @@ __host__ __device__ inline size_t resident_smem_bytes(long long R, long long n, 
          size_t(R) * kRW * 8 + size_t(R) * 16 + (sets > 1 ? size_t(sets) * ld * 8 : 0) + 64;
 }
 
-template <typename T, bool CLUSTER>
+// TG: storage type of C / X in global memory; T: type of the shared-memory
+// tiles. fp32 storage may run on fp64 tiles (when they fit): the iteration is
+// then the reference's fp64 arithmetic and X is rounded to fp32 only when the
+// launch writes the plan back.
+template <typename T, bool CLUSTER, typename TG = T>
 __global__ void __launch_bounds__(kRT, 1) resident_kernel(ResidentArgs A) {
   namespace cg = cooperative_groups;
   using V = typename Vec<T>::type;
@@ -95,8 +101,8 @@ __global__ void __launch_bounds__(kRT, 1) resident_kernel(ResidentArgs A) {
   if (ctl->done) return;  // uniform per problem
   const long long m = A.m, n = A.n, ld = A.ld;
   const int R = A.R;
-  T* Xg = static_cast<T*>(A.X) + prob * A.mat_stride;
-  const T* Cg = static_cast<const T*>(A.C) + prob * A.mat_stride;
+  TG* Xg = static_cast<TG*>(A.X) + prob * A.mat_stride;
+  const TG* Cg = static_cast<const TG*>(A.C) + prob * A.mat_stride;
   double* phi = A.phi + prob * m;
   double* av = A.a + prob * m;
   double* rv = A.r + prob * m;
@@ -162,13 +168,30 @@ __global__ void __launch_bounds__(kRT, 1) resident_kernel(ResidentArgs A) {
   // load the tiles (once per solve)
   {
     const long long elems = (long long)nr * ld;
-    const V* cs = reinterpret_cast<const V*>(Cg + i0 * ld);
-    const V* xs = reinterpret_cast<const V*>(Xg + i0 * ld);
-    V* cd = reinterpret_cast<V*>(Ct);
-    V* xd = reinterpret_cast<V*>(Xt);
-    for (long long t = threadIdx.x; t < elems / VEC; t += kRT) {
-      cd[t] = cs[t];
-      xd[t] = xs[t];
+    if constexpr (std::is_same<T, TG>::value) {
+      const V* cs = reinterpret_cast<const V*>(Cg + i0 * ld);
+      const V* xs = reinterpret_cast<const V*>(Xg + i0 * ld);
+      V* cd = reinterpret_cast<V*>(Ct);
+      V* xd = reinterpret_cast<V*>(Xt);
+      for (long long t = threadIdx.x; t < elems / VEC; t += kRT) {
+        cd[t] = cs[t];
+        xd[t] = xs[t];
+      }
+    } else {  // widen (exact)
+      using VG = typename Vec<TG>::type;
+      constexpr int VG_N = Vec<TG>::N;
+      const VG* cs = reinterpret_cast<const VG*>(Cg + i0 * ld);
+      const VG* xs = reinterpret_cast<const VG*>(Xg + i0 * ld);
+      for (long long t = threadIdx.x; t < elems / VG_N; t += kRT) {
+        double cw[VG_N], xw[VG_N];
+        unpack(cs[t], cw);
+        unpack(xs[t], xw);
+#pragma unroll
+        for (int e = 0; e < VG_N; ++e) {
+          Ct[t * VG_N + e] = (T)cw[e];
+          Xt[t * VG_N + e] = (T)xw[e];
+        }
+      }
     }
     for (long long j = threadIdx.x; j < n; j += kRT) psi_s[j] = psi[j];
     for (int t = threadIdx.x; t < nr; t += kRT) phi_s[t] = phi[i0 + t];
@@ -434,9 +457,21 @@ __global__ void __launch_bounds__(kRT, 1) resident_kernel(ResidentArgs A) {
   // write back the plan, phi and r of own rows (psi, s, b, a already global)
   {
     const long long elems = (long long)nr * ld;
-    V* xd = reinterpret_cast<V*>(Xg + i0 * ld);
-    const V* xs = reinterpret_cast<const V*>(Xt);
-    for (long long t = threadIdx.x; t < elems / VEC; t += kRT) xd[t] = xs[t];
+    if constexpr (std::is_same<T, TG>::value) {
+      V* xd = reinterpret_cast<V*>(Xg + i0 * ld);
+      const V* xs = reinterpret_cast<const V*>(Xt);
+      for (long long t = threadIdx.x; t < elems / VEC; t += kRT) xd[t] = xs[t];
+    } else {  // round to the storage type (the plan's only rounding in this launch)
+      using VG = typename Vec<TG>::type;
+      constexpr int VG_N = Vec<TG>::N;
+      VG* xd = reinterpret_cast<VG*>(Xg + i0 * ld);
+      for (long long t = threadIdx.x; t < elems / VG_N; t += kRT) {
+        double o[VG_N];
+#pragma unroll
+        for (int e = 0; e < VG_N; ++e) o[e] = (double)Xt[t * VG_N + e];
+        xd[t] = pack<TG>(o);
+      }
+    }
     for (int t = threadIdx.x; t < nr; t += kRT) {
       phi[i0 + t] = phi_s[t];
       rv[i0 + t] = r_s[t];

@@ -423,7 +423,10 @@ def test_gl_fused_and_trace_match_unfused(ora):
                                       (5, 3000, "none"), (1500, 1400, "quad")])
 def test_resident_matches_streaming(ora, monkeypatch, storage, m, n, kind):
     """The on-chip resident loop (grid mode) and the streaming graph loop give
-    the same trajectory (same element-wise arithmetic; reduction order only)."""
+    the same trajectory: fp64 storage -- same element-wise arithmetic,
+    reduction order only; fp32 storage -- the resident loop runs on fp64
+    shared-memory tiles (X rounded to fp32 only at write-back), so the two
+    agree to the fp32 contract (1e-5)."""
     C, p, q, *_ = ora.gaussian_problem(m, n, 2)
     reg = otdr.QuadraticReg(5e-3 * (m + n)) if kind == "quad" else otdr.ZeroReg()
     out = {}
@@ -440,10 +443,10 @@ def test_resident_matches_streaming(ora, monkeypatch, storage, m, n, kind):
         out[mode] = (st, rep)
         eng.close()
     a, b = out["on"], out["off"]
-    tol = 1e-12 if storage == "f64" else 1e-6
+    tol = 1e-12 if storage == "f64" else 1e-5
     assert a[0].k == b[0].k == 37
     assert rel(a[0].X, b[0].X) <= tol and rel(a[0].phi, b[0].phi) <= tol and rel(a[0].psi, b[0].psi) <= tol
-    assert abs(a[0].theta - b[0].theta) <= 1e-12 * max(1, abs(b[0].theta))
+    assert abs(a[0].theta - b[0].theta) <= (1e-12 if storage == "f64" else 1e-6) * max(1, abs(b[0].theta))
     assert a[1].termination == b[1].termination
     assert abs(a[1].iterations - b[1].iterations) <= (0 if storage == "f64" else 2)
     assert abs(a[1].objective - b[1].objective) <= (1e-9 if storage == "f64" else 1e-6) * abs(b[1].objective)
@@ -1149,3 +1152,31 @@ def test_tstream_geometries_match_oracle(ora, monkeypatch, ts_cfg, m, n):
     assert abs(rep.iterations - o.iterations) <= 2
     assert abs(rep.objective - o.objective) <= 1e-6 * max(abs(o.objective), 1e-300)
     eng.close()
+
+
+@pytest.mark.parametrize("m,n,kind", [(20, 20, "none"), (300, 517, "quad"), (1000, 1000, "quad")])
+def test_resident_f32_storage_runs_fp64_tiles(ora, m, n, kind):
+    """fp32 storage on the resident loop: the iteration runs on fp64 tiles of
+    the fp32-rounded cost, so after k steps in one launch the state equals the
+    oracle's fp64 DR on that cost up to the final fp32 rounding of X (and
+    phi / psi to fp64 reduction order)."""
+    C, p, q, *_ = ora.gaussian_problem(m, n, 2)
+    pr = ora.Problem(C.astype(np.float32).astype(np.float64), p, q)
+    alpha = 5e-3 * (m + n)
+    oreg = oracle_reg(ora, kind, alpha, None, n)
+    st = ora.make_state(pr)
+    eng = otdr.Engine(m, n, "f32")
+    eng.set_problem(C, p, q)
+    eng.set_regularizer(dev_reg(kind, alpha, None, n))
+    eng.set_state()
+    assert eng.solve_path() == "resident"
+    assert "f64 tiles" in eng.kernel_name()
+    rho = ora.default_stepsize(m, n)
+    for _ in range(37):
+        ora.step(st, pr, oreg, rho)
+    eng.step(rho, 37)
+    g = eng.get_state()
+    eng.close()
+    assert rel(g.X, st.X) <= 1e-7
+    for nm in ("phi", "psi", "a", "b"):
+        assert rel(getattr(g, nm), getattr(st, nm)) <= 1e-10, nm
